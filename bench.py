@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""bench.py -- oriented edges/s of an exact triangle count on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A step of `value` is one count of the whole graph (count_triangles_seq: the
+middle-vertex engine's plan + engine kernels) with the oriented CSR resident
+in HBM; metric = m / step time.  `e2e` is the same metric through the public
+API with host buffers: pinned raw edge list -> H2D -> normalize ->
+build_graph -> count -> D2H of the count, every step.  The reference arm
+(--impl reference) times the reference's CPU algorithm (the C restatement in
+oracle/, all host threads, the count_dynamic task queue) on a bounded
+sample of the same workload.
+
+N > 1 (torchrun, one rank per GPU): every rank builds the graph, owns a
+contiguous middle-vertex range balanced by the engine's cost prefix and the
+per-GPU uint64 counts are combined with an NCCL all-reduce inside the timed
+region; timing is the max over ranks ("strong" scaling: total work fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "oriented edges/s (exact triangle count)"
+UNIT = "edges/s"
+HBM_FALLBACK_GBS = 6650.0
+
+CONFIGS = {
+    "cfg1": dict(kind="er", n=16384, m=131072, seed=1,
+                 desc="cfg1 ER G(n=16384, m=131072 uniform pairs) seed=1 (device generator)"),
+    "cfg2": dict(kind="pa", n=1_000_000, d=100, seed=1,
+                 desc="cfg2 BA/PA n=1,000,000 d=100 (50 distinct degree-proportional targets) seed=1 "
+                      "(reference generate_pa, bit-identical)"),
+    "cfg4s20": dict(kind="rmat", scale=20, ef=32, seed=1,
+                    desc="R-MAT scale 20 edge factor 32 (.57,.19,.19,.05) seed=1 (cfg4 family, reduced scale)"),
+    "cfg5": dict(kind="er", n=2_000_000, m=400_000_000, seed=1,
+                 desc="cfg5 dense ER n=2,000,000, 400M uniform pairs seed=1 (device generator)"),
+}
+
+
+# ----------------------------------------------------------------- helpers
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    for p in (os.path.join(REPO, "MEASURED_PEAKS.json"), "/root/repo/MEASURED_PEAKS.json"):
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            continue
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ----------------------------------------------------------------- workloads
+
+def host_raw_edges(cfg, pin):
+    """The workload's raw edge list in (pinned) host memory, int32 (m_raw, 2)."""
+    import torch
+
+    import paper_1406_5687_b200 as tcb
+    from paper_1406_5687_b200.graph_io import er_edges, pa_edges_host, rmat_edges
+
+    c = CONFIGS[cfg]
+    if c["kind"] == "pa":
+        return pa_edges_host(tcb.PaParams(c["n"], c["d"], c["seed"]), pin=pin)
+    dev = er_edges(c["n"], c["m"], c["seed"]) if c["kind"] == "er" else rmat_edges(c["scale"], c["ef"], c["seed"])
+    out = torch.empty(tuple(dev.shape), dtype=torch.int32, pin_memory=pin)
+    out.copy_(dev)
+    del dev
+    return out
+
+
+def oracle_raw_edges(cfg):
+    """Reference-arm input: built without any product kernel."""
+    from oracle import gen_twin
+    from oracle import oracle as O
+
+    c = CONFIGS[cfg]
+    if c["kind"] == "pa":
+        return O.pa_edge_list(c["n"], c["d"], c["seed"])
+    if c["kind"] == "er":
+        return gen_twin.er_gnm(c["n"], c["m"], c["seed"]).astype(np.int64)
+    return gen_twin.rmat(c["scale"], c["ef"], c["seed"]).astype(np.int64)
+
+
+# ----------------------------------------------------------------- CPU arm
+
+def cpu_count_sample(indptr, indices, n, target_s, threads, block=256):
+    """Times the reference algorithm (oracle C port of count_node_range, tasks
+    pulled from a shared atomic counter by `threads` host threads) on a
+    strided sample of node blocks sized to take about target_s seconds.
+    Returns (edges/s, seconds, sample_edges, stride, triangles)."""
+    from oracle import oracle as O
+
+    nblocks = (n + block - 1) // block
+    deg = np.diff(indptr)
+
+    def run(stride):
+        starts = np.arange(0, nblocks, stride, dtype=np.int64) * block
+        lens = np.minimum(block, n - starts)
+        edges = int(sum(int(deg[s:s + l].sum()) for s, l in zip(starts, lens)))
+        t0 = time.perf_counter()
+        tri = O.count_tasks_threaded(indptr, indices, starts, lens, threads)
+        return time.perf_counter() - t0, edges, tri
+
+    probe_stride = max(1, min(64, nblocks))
+    t, e, _ = run(probe_stride)
+    est_full = t * probe_stride
+    stride = max(1, int(round(est_full / max(target_s, 1e-3))))
+    stride = min(stride, nblocks)
+    t, e, tri = run(stride)
+    return e / t, t, e, stride, tri
+
+
+def reference_arm(args):
+    import torch.distributed as dist  # noqa: F401
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    raw = oracle_raw_edges(args.config)
+    n, e = O.normalize(raw)
+    g = O.build_graph(n, e, full=False)
+    log(f"[reference] oracle build {time.perf_counter() - t0:.1f}s n={g.n} m={g.m} threads={threads}")
+    per_step = max(1.0, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        r, t, edges, stride, tri = cpu_count_sample(g.eff_indptr, g.eff_indices, g.n, per_step, threads)
+        if i >= args.warmup:
+            rates.append(r)
+            info = (t, edges, stride)
+    value = statistics.median(rates)
+    t, edges, stride = info
+    sample = (f"every {stride}-th block of 256 canonical nodes ({edges} oriented edges, "
+              f"{100.0 * edges / g.m:.1f}% of m), count_node_range per block on a shared atomic task queue")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config]["desc"], "n": g.n, "m": g.m},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-target-s", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: --warmup < 3 is below the timing contract; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return run_ours(args)
+
+
+def run_ours(args):
+    line = _gpu_arm_core(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def _gpu_arm_core(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1406_5687_b200 as tcb
+    from paper_1406_5687_b200 import _lib
+    from paper_1406_5687_b200.partitioning import balanced_bounds
+    from paper_1406_5687_b200.sequential import count_middle
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.perf_counter()
+    raw_host = host_raw_edges(args.config, pin=True)
+    m_raw = int(raw_host.shape[0])
+    log(f"[ours r{rank}] generated {m_raw} raw pairs in {time.perf_counter() - t0:.1f}s")
+
+    tb = time.perf_counter()
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw_host)))
+    torch.cuda.synchronize()
+    log(f"[ours r{rank}] first build n={g.n} m={g.m} in {time.perf_counter() - tb:.2f}s")
+    n, m = g.n, g.m
+    W = int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum())
+
+    if world > 1:
+        ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
+        ub = balanced_bounds(ucost, 0, n, world).cpu().numpy()
+        u0, u1 = int(ub[rank]), int(ub[rank + 1])
+    else:
+        u0, u1 = 0, n
+    out = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def count_step():
+        count_middle(g, u0, u1, out=out)
+        if world > 1:
+            dist.all_reduce(out)
+        return out
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        count_step()
+    barrier()
+    T = int(count_step().item())
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(1)
+            starts[i].record()
+            r = count_step()
+            ends[i].record()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = max_over_ranks(sum(step_ms) / len(step_ms))
+    if int(r.item()) != T:
+        raise RuntimeError("count changed between steps")
+
+    # dominant kernel (the engine) timed with CUDA events on its own stream
+    _lib.lib().tc_engine_timing(1, None, None)
+    for _ in range(args.steps):
+        flush.fill_(1)
+        count_step()
+    torch.cuda.synchronize()
+    tot, nl = ctypes.c_double(), ctypes.c_longlong()
+    _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl))
+    engine_ms = max_over_ranks(tot.value / max(1, nl.value))
+
+    e2e_ms = None
+    if not args.no_e2e:
+        del g
+        torch.cuda.empty_cache()
+        samples = []
+        for i in range(args.warmup + args.steps):
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            dev_raw = raw_host.to(dev, non_blocking=True)
+            gg = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=dev_raw)))
+            if world > 1:
+                c = count_middle(gg, u0, u1)
+                dist.all_reduce(c)
+                tri = int(c.item())
+            else:
+                tri = tcb.count_triangles_seq(gg)
+            e.record()
+            torch.cuda.synchronize()
+            if tri != T:
+                raise RuntimeError("e2e count mismatch")
+            if i >= args.warmup:
+                samples.append(s.elapsed_time(e))
+            del gg, dev_raw
+        e2e_ms = max_over_ranks(sum(samples) / len(samples))
+
+    clock_summary = clocks.summary()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_leg(raw_host, args.cpu_target_s)
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": UNIT, "error": repr(exc)}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+
+    peak, peak_src = measured_peak()
+    b_alg = 4 * W + 20 * m + 8 * (n + 1)
+    achieved = b_alg / (engine_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", f"ncu_engine_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": m / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded generator; no dataset)",
+        "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw,
+                   "triangles": T, "W_succsum": W,
+                   "l2": "inputs > L2 (rev_seg 16 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
+                   "parallelism": f"middle-vertex ranges x{world}" + (" + NCCL all-reduce" if world > 1 else "")},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_engine<PullSegs> (middle-vertex engine)",
+                     "bytes_model": "B_alg = 4W + 20m + 8(n+1) per launch (SURVEY §8(d) merge model)",
+                     "kernel_ms": engine_ms, "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": None if e2e_ms is None else {
+            "value": m / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": m_raw * 8,
+            "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
+            "path": "pinned host raw pairs -> H2D -> normalize -> build_graph -> count_triangles_seq -> D2H"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clock_summary,
+    }
+    return line
+
+
+def cpu_baseline_leg(raw_host, target_s):
+    """Reference algorithm on the host cores, same workload (oracle port)."""
+    from oracle import oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    n, e = O.normalize(raw_host.numpy().astype(np.int64))
+    g = O.build_graph(n, e, full=False)
+    log(f"[cpu] oracle build {time.perf_counter() - t0:.1f}s")
+    rate, t, edges, stride, _ = cpu_count_sample(g.eff_indptr, g.eff_indices, g.n, target_s, threads)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"every {stride}-th block of 256 canonical nodes ({edges} oriented edges, "
+                      f"{100.0 * edges / g.m:.1f}% of m) in {t:.2f}s; oracle C restatement of "
+                      "count_node_range on a shared atomic task queue"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

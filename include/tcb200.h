@@ -1,0 +1,206 @@
+/*
+ * tcb200.h -- C ABI of libtcb200.so, the B200-native (sm_100a) exact triangle
+ * counter.  Drop-in replacement for the native boundary of the reference
+ * `tricount` package (/root/reference/pkg/src/tricount): the numba kernels
+ * of _kernels.py and the numpy construction of graph.py / partitioning.py.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer unless its name ends in
+ *     `_host`.  The library never frees caller memory; scratch is
+ *     stream-ordered (cudaMallocAsync) and released before return.
+ *   - Node ids are int32, CSR offsets int64, counts uint64 (the reference
+ *     uses int64 everywhere, graph.py:85,111,120).
+ *   - `stream` is a cudaStream_t (0 = legacy default stream).  Calls are
+ *     stream-ordered; a call that returns host scalars (`*_host`)
+ *     synchronises the stream before returning.
+ *   - Return 0 (TC_OK) or a negative status; tc_last_error() describes the
+ *     last failure on the calling thread.  The Python layer maps
+ *     TC_EINVAL -> ValueError, TC_EINDEX -> IndexError, others ->
+ *     RuntimeError, mirroring the reference's exceptions.
+ *   - Thread-safe across host threads using distinct streams (the reference's
+ *     kernels are nogil and called concurrently from rank threads,
+ *     _kernels.py:12, runtime.py:420-454).
+ */
+#ifndef TCB200_H
+#define TCB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* tc_stream_t; /* cudaStream_t */
+
+enum {
+  TC_OK = 0,
+  TC_EINVAL = -1, /* ValueError in the reference */
+  TC_EINDEX = -2, /* IndexError */
+  TC_ECUDA = -3,  /* CUDA runtime failure */
+  TC_ENOMEM = -4  /* device allocation failure */
+};
+
+/* Cost kinds, CostKind order (partitioning.py:32-35). */
+enum { TC_COST_UNIT = 0, TC_COST_DEGREE = 1, TC_COST_SUCC_SUM = 2, TC_COST_PRED_SUM = 3 };
+
+const char* tc_last_error(void);
+int tc_abi_version(void);
+/* Releases pooled scratch back to the driver (between large jobs). */
+int tc_trim_pool(void);
+
+/* ---------------------------------------------------------------- build */
+
+/* normalize (graph.py:76-103): drop self-loops, first-seen compaction of
+ * non-dense labels, dedup undirected pairs; output sorted (lo, hi) pairs.
+ * edges: int32[2*m_raw] (u0,v0,u1,v1,...), labels >= 0 else TC_EINVAL.
+ * out_edges: int32[2*m_raw] capacity.  Synchronises (returns m, n). */
+int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges,
+                 int64_t* m_host, int64_t* n_host, tc_stream_t stream);
+
+/* build_graph + _assemble (graph.py:106-153): degree order (ascending
+ * (deg, id), graph.py:152) unless `order` (int32[n], order[i] = original id
+ * at canonical position i) is given (the _build_graph_input_order hook,
+ * graph.py:156-160).  Edge ids must lie in [0, n) (else TC_EINDEX).
+ * Outputs (all caller-allocated):
+ *   eff_indptr int64[n+1], eff_indices int32[m]      forward CSR N^_v
+ *   relabel, orig_ids, deg, eff_deg  int32[n]
+ *   rev_indptr int64[n+1]   predecessors of u (v with u in N^_v), by v
+ *   rev_src    int32[m]     the predecessor v
+ *   rev_seg    int64[2*m]   (e+1, eff_indptr[v+1]): suffix of N^_v after u
+ *   rev_cost   int64[n+1]   exclusive prefix over u of the pull-engine cost
+ * Asynchronous. */
+int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
+                   int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
+                   int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
+                   int32_t* rev_src, int64_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
+
+/* Full CSR (graph.py:125-127) assembled from the forward and reverse CSRs:
+ * row u = predecessors (ascending) then N^_u.  full_indptr int64[n+1],
+ * full_indices int32[2m]. */
+int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
+                  const int64_t* rev_indptr, const int32_t* rev_src, int64_t n,
+                  int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream);
+
+/* ---------------------------------------------------------------- count */
+
+/* Middle-vertex ("pull") engine: triangles v < u < w whose middle vertex u
+ * lies in [u0, u1), written to out[bucket(u)] (uint64).  bucket_bounds
+ * (int64[nbuckets+1], ascending) bins u; NULL with nbuckets==1 sums all.
+ * Table lists N^_u come from (tab_indptr, tab_indices) indexed by u;
+ * predecessor suffixes are rev_seg pairs indexing `pool` (int32).
+ * On one GPU pool == eff_indices.  out is overwritten (not accumulated).
+ * This is count_node_range(0, n) (_kernels.py:40-52) for the whole range,
+ * and the per-rank partials of count_space_surrogate for rank buckets. */
+int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
+                    const int64_t* rev_indptr, const int64_t* rev_seg,
+                    const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
+                    int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                    unsigned long long* out, tc_stream_t stream);
+
+/* Lowest-vertex ("push") engine: count_node_range(v0, v1)
+ * (_kernels.py:40-52) with per-bucket partials: out[b] = triangles whose
+ * lowest vertex lies in [bucket_bounds[b], bucket_bounds[b+1]).
+ * bucket_bounds NULL with nbuckets==1 means the single range [v0, v1). */
+int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n,
+                    int64_t v0, int64_t v1, const int64_t* bucket_bounds, int32_t nbuckets,
+                    unsigned long long* out, tc_stream_t stream);
+
+/* Engine timing (measurement only): reports the accumulated device time and
+ * launch count of engine kernels since the last reset, then, if enable >= 0,
+ * resets the counters and turns CUDA-event bracketing of every engine
+ * launch on (1) or off (0).  Bracketing synchronises after each launch. */
+int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host);
+
+/* |a ∩ b| of two strictly ascending int32 lists (_kernels.py:15-37). */
+int tc_intersect_count(const int32_t* a, int64_t na, const int32_t* b, int64_t nb,
+                       unsigned long long* out, tc_stream_t stream);
+
+/* Dense-bitmap brute-force count over the full CSR, n <= 2000
+ * (sequential.py:37-51); independent of the engines above. */
+int tc_count_brute(const int64_t* full_indptr, const int32_t* full_indices, int64_t n,
+                   unsigned long long* out, tc_stream_t stream);
+
+/* ---------------------------------------------------------- partitioning */
+
+/* node_costs (partitioning.py:79-92) -> int64[n]. */
+int tc_node_costs(int32_t kind, const int64_t* eff_indptr, const int32_t* eff_indices,
+                  const int32_t* deg, const int32_t* eff_deg, int64_t n, int64_t* out,
+                  tc_stream_t stream);
+
+/* balanced_ranges (partitioning.py:95-122): bounds int64[k+1] (device)
+ * for `costs` restricted to [start, start+count). */
+int tc_balanced_bounds(const int64_t* costs, int64_t start, int64_t count, int64_t k,
+                       int64_t* bounds, tc_stream_t stream);
+
+/* plan_tasks (dynamic_lb.py:68-109).  initial_bounds int64[nranks]
+ * (P-1 ranges), queue_v/queue_t int64[n] capacity, targets f64[n].
+ * Synchronises (returns split, nqueue, total). */
+int tc_plan_tasks(const int64_t* costs, int64_t n, int64_t nranks, int64_t* initial_bounds,
+                  int64_t* queue_v, int64_t* queue_t, double* targets, int64_t* split_host,
+                  int64_t* nqueue_host, int64_t* total_host, tc_stream_t stream);
+
+/* Surrogate census (scan_for_surrogate's LastProc records,
+ * _kernels.py:94-126): census int64[P*P], census[i*P+j] = number of owned
+ * v of rank i whose N^_v has an id owned by j != i.  words int64[P] =
+ * sum over those records of (2 + d^_v) (runtime.py:80-86 wire model). */
+int tc_surrogate_census(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n,
+                        const int64_t* bounds, int32_t P, long long* census, long long* words,
+                        tc_stream_t stream);
+
+/* Owner-change records of one rank (the send list of the surrogate push):
+ * for owned v in [bounds[rank], bounds[rank+1]) emits one (v, dest) per
+ * remote rank dest > rank touched by N^_v, grouped by dest ascending then v
+ * ascending.  rec_v/rec_dest int32[cap]; counts int64[P] per dest.
+ * Synchronises (returns the record count). */
+int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n,
+                         const int64_t* bounds, int32_t P, int32_t rank, int32_t* rec_v,
+                         int32_t* rec_dest, int64_t cap, long long* counts,
+                         int64_t* nrec_host, tc_stream_t stream);
+
+/* Packs the N^_v lists of records [r0, r1) into one send buffer:
+ * out_len int64[r1-r0] list lengths, out_ids int32[...] concatenated lists,
+ * out_v int32[r1-r0] node ids.  out_offsets int64[r1-r0+1] (device) must
+ * hold the exclusive prefix of lengths (see tc_surrogate_pack_sizes). */
+int tc_surrogate_pack_sizes(const int64_t* eff_indptr, const int32_t* rec_v, int64_t nrec,
+                            int64_t* out_offsets, int64_t* total_host, tc_stream_t stream);
+int tc_surrogate_pack(const int64_t* eff_indptr, const int32_t* eff_indices,
+                      const int32_t* rec_v, int64_t nrec, const int64_t* offsets,
+                      int32_t* out_ids, tc_stream_t stream);
+
+/* Pull-engine segments from neighbour lists (surrogate_count_list,
+ * _kernels.py:70-80, re-expressed): for list l = ids[off[l], off[l+1]) and
+ * every position k holding an owned id u in [lo, hi) with a non-empty
+ * suffix, emits owner[i] = u - lo and segs[2i..2i+1] =
+ * (pool_base + k + 1, pool_base + off[l+1]).  Works for the local shard's
+ * own rows and for received lists alike.  owner == NULL only counts.
+ * Synchronises (returns the segment count; order is unspecified). */
+int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int64_t nl,
+                      int64_t lo, int64_t hi, int64_t pool_base, int32_t* owner, int64_t* segs,
+                      int64_t cap, int64_t* nseg_host, tc_stream_t stream);
+
+/* Groups segments by owner into a CSR usable by tc_count_middle:
+ * row_indptr int64[n_owner+1], row_segs int64[2*nseg], cost_prefix
+ * int64[n_owner+1] (pull-engine cost, needs the table CSR tab_indptr). */
+int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int64_t n_owner,
+                    const int64_t* tab_indptr, int64_t* row_indptr, int64_t* row_segs,
+                    int64_t* cost_prefix, tc_stream_t stream);
+
+/* ------------------------------------------------------------ generators */
+
+/* ER G(n,m) raw pairs (configs 1, 5): out int32[2m]. */
+int tc_gen_er(int64_t n, int64_t m, uint64_t seed, int32_t* out, tc_stream_t stream);
+/* R-MAT raw pairs (config 4): 2^scale*edge_factor samples, (.57,.19,.19,.05). */
+int tc_gen_rmat(int32_t scale, int64_t edge_factor, uint64_t seed, int32_t* out,
+                tc_stream_t stream);
+/* Preferential attachment, bit-identical to the reference's pa_edge_list
+ * (_kernels.py:129-178; sequential by construction, runs on the host).
+ * out_host int32[2*tc_pa_num_edges(n,k)] as (src, dst) pairs. */
+int64_t tc_pa_num_edges(int64_t n, int64_t k);
+int tc_gen_pa_host(int64_t n, int64_t k, uint64_t seed, int32_t* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCB200_H */

@@ -1,0 +1,107 @@
+"""ctypes binding of libtcb200.so (the C ABI declared in include/tcb200.h).
+
+The product has no CPU fallback: if the shared library is missing or no CUDA
+device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libtcb200.so")
+_LIB = None
+
+TC_OK, TC_EINVAL, TC_EINDEX, TC_ECUDA, TC_ENOMEM = 0, -1, -2, -3, -4
+
+_i64, _i32, _u64, _vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+# name -> argtypes (every device pointer / stream is passed as c_void_p)
+_SIGS = {
+    "tc_abi_version": [],
+    "tc_trim_pool": [],
+    "tc_normalize": [_vp, _i64, _vp, _pi64, _pi64, _vp],
+    "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_build_full": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
+    "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
+    "tc_intersect_count": [_vp, _i64, _vp, _i64, _vp, _vp],
+    "tc_engine_timing": [_i32, _vp, _vp],
+    "tc_count_brute": [_vp, _vp, _i64, _vp, _vp],
+    "tc_node_costs": [_i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp],
+    "tc_balanced_bounds": [_vp, _i64, _i64, _i64, _vp, _vp],
+    "tc_plan_tasks": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _pi64, _vp],
+    "tc_surrogate_census": [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
+    "tc_surrogate_records": [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _vp, _i64, _vp, _pi64, _vp],
+    "tc_surrogate_pack_sizes": [_vp, _vp, _i64, _vp, _pi64, _vp],
+    "tc_surrogate_pack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "tc_owner_segments": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _pi64, _vp],
+    "tc_segments_csr": [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
+    "tc_gen_er": [_i64, _i64, _u64, _vp, _vp],
+    "tc_gen_rmat": [_i32, _i64, _u64, _vp, _vp],
+    "tc_pa_num_edges": [_i64, _i64],
+    "tc_gen_pa_host": [_i64, _i64, _u64, _vp],
+}
+EXPORTED = sorted(_SIGS) + ["tc_last_error"]
+
+
+def build_library(force=False):
+    """Compile libtcb200.so in-tree (nvcc, sm_100a)."""
+    if force or not os.path.exists(_SO):
+        subprocess.run(["make", "-s", "-j8", "-C", _HERE], check=True)
+    return _SO
+
+
+def lib():
+    """Load the library (build it first if absent)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(_SO):
+            build_library()
+        L = ctypes.CDLL(_SO)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = _i64 if name == "tc_pa_num_edges" else ctypes.c_int
+        L.tc_last_error.argtypes = []
+        L.tc_last_error.restype = ctypes.c_char_p
+        _LIB = L
+    return _LIB
+
+
+def check(rc):
+    if rc == TC_OK:
+        return
+    msg = lib().tc_last_error().decode(errors="replace")
+    if rc == TC_EINVAL:
+        raise ValueError(msg)
+    if rc == TC_EINDEX:
+        raise IndexError(msg)
+    raise RuntimeError(f"libtcb200 error {rc}: {msg}")
+
+
+def call(name, *args):
+    check(getattr(lib(), name)(*args))
+
+
+def device():
+    """The CUDA device the product runs on; raises loudly without one."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1406_5687_b200 needs a CUDA device (B200); no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())

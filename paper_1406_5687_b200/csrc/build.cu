@@ -1,0 +1,572 @@
+// build.cu -- device graph construction: normalize, degree ordering,
+// orientation, forward / reverse / full CSR, node costs.
+//
+// Restates graph.py:76-153 and partitioning.py:79-92 of the reference with
+// device radix sorts (CUB onesweep), atomic histograms and boundary-search
+// CSR builds.  Every sort is stable, which is what makes the outputs
+// bit-identical to numpy's stable lexsort / unique.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace tcb {
+
+static constexpr uint32_t kInf32 = 0xFFFFFFFFu;
+static constexpr int kBlock = 256;
+
+// Pull-engine cost model (count.cu reads it through rev_cost): per
+// predecessor segment its length plus kSegCost, per table build d^_u plus
+// kTabCost; zero for u without successors (the engine skips them).
+static constexpr int64_t kSegCost = 2;
+static constexpr int64_t kTabCost = 16;
+
+// ---------------------------------------------------------------- kernels
+
+__global__ void k_minmax(const int32_t* __restrict__ a, int64_t cnt, int* mn, int* mx) {
+  int lo = INT_MAX, hi = INT_MIN;
+  GRID_STRIDE(i, cnt) {
+    int x = a[i];
+    lo = min(lo, x);
+    hi = max(hi, x);
+  }
+  typedef cub::BlockReduce<int, kBlock> R;
+  __shared__ typename R::TempStorage t1, t2;
+  int blo = R(t1).Reduce(lo, cub::Min());
+  int bhi = R(t2).Reduce(hi, cub::Max());
+  if (threadIdx.x == 0) {
+    atomicMin(mn, blo);
+    atomicMax(mx, bhi);
+  }
+}
+
+struct NotSelfLoop {
+  __host__ __device__ bool operator()(const unsigned long long& x) const {
+    return (uint32_t)(x & 0xFFFFFFFFull) != (uint32_t)(x >> 32);
+  }
+};
+
+__global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t cnt, uint32_t* fp) {
+  GRID_STRIDE(i, cnt) atomicMin(&fp[ids[i]], (uint32_t)i);
+}
+
+// K = number of present labels, Lf = largest present label.
+__global__ void k_present(const uint32_t* __restrict__ fp, int64_t L1,
+                          unsigned long long* count, int* maxid) {
+  unsigned long long c = 0;
+  int mx = -1;
+  GRID_STRIDE(i, L1) {
+    if (fp[i] != kInf32) {
+      ++c;
+      mx = max(mx, (int)i);
+    }
+  }
+  typedef cub::BlockReduce<unsigned long long, kBlock> R1;
+  typedef cub::BlockReduce<int, kBlock> R2;
+  __shared__ typename R1::TempStorage t1;
+  __shared__ typename R2::TempStorage t2;
+  unsigned long long bc = R1(t1).Sum(c);
+  int bm = R2(t2).Reduce(mx, cub::Max());
+  if (threadIdx.x == 0) {
+    atomicAdd(count, bc);
+    atomicMax(maxid, bm);
+  }
+}
+
+struct IsPresent {
+  const uint32_t* fp;
+  __host__ __device__ bool operator()(const int& i) const { return fp[i] != 0xFFFFFFFFu; }
+};
+
+__global__ void k_gather_u32(const int32_t* __restrict__ idx, const uint32_t* __restrict__ src,
+                             int64_t cnt, uint32_t* out) {
+  GRID_STRIDE(i, cnt) out[i] = src[idx[i]];
+}
+
+__global__ void k_rank_scatter(const int32_t* __restrict__ ids, int64_t cnt, int32_t* new_id) {
+  GRID_STRIDE(i, cnt) new_id[ids[i]] = (int32_t)i;
+}
+
+__global__ void k_remap(int32_t* ids, int64_t cnt, const int32_t* __restrict__ new_id) {
+  GRID_STRIDE(i, cnt) ids[i] = new_id[ids[i]];
+}
+
+// (min, max) of each pair packed as lo << b | hi; optional relabel map.
+__global__ void k_pack_pairs(const int32_t* __restrict__ e, int64_t m,
+                             const int32_t* __restrict__ relabel, int b,
+                             unsigned long long* keys) {
+  GRID_STRIDE(i, m) {
+    int32_t x = e[2 * i], y = e[2 * i + 1];
+    if (relabel) {
+      x = relabel[x];
+      y = relabel[y];
+    }
+    uint32_t lo = (uint32_t)min(x, y), hi = (uint32_t)max(x, y);
+    keys[i] = ((unsigned long long)lo << b) | hi;
+  }
+}
+
+__global__ void k_unpack_pairs(const unsigned long long* __restrict__ keys, int64_t m, int b,
+                               int32_t* out) {
+  unsigned long long mask = (1ull << b) - 1;
+  GRID_STRIDE(i, m) {
+    unsigned long long k = keys[i];
+    out[2 * i] = (int32_t)(k >> b);
+    out[2 * i + 1] = (int32_t)(k & mask);
+  }
+}
+
+__global__ void k_histogram(const int32_t* __restrict__ ids, int64_t cnt, int32_t* h) {
+  GRID_STRIDE(i, cnt) atomicAdd(&h[ids[i]], 1);
+}
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+  GRID_STRIDE(i, n) a[i] = (int32_t)i;
+}
+
+__global__ void k_copy_i32(const int32_t* __restrict__ a, int32_t* b, int64_t n) {
+  GRID_STRIDE(i, n) b[i] = a[i];
+}
+
+__global__ void k_range_check(const int32_t* __restrict__ ids, int64_t cnt, int64_t n, int* bad) {
+  GRID_STRIDE(i, cnt) {
+    int x = ids[i];
+    if (x < 0) atomicOr(bad, 1);
+    else if ((int64_t)x >= n) atomicOr(bad, 2);
+  }
+}
+
+// Per-row entry counts from row keys sorted ascending: the first entry of a
+// row subtracts its index, the last adds index+1 (two uncontended atomics
+// per non-empty row); an exclusive scan then gives the CSR offsets.
+template <class RowOf>
+__global__ void k_row_counts(RowOf row_of, int64_t m, long long* cnt) {
+  GRID_STRIDE(i, m) {
+    int64_t r = row_of(i);
+    if (i == 0 || row_of(i - 1) != r) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[r]), (unsigned long long)(-(long long)i));
+    if (i == m - 1 || row_of(i + 1) != r) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[r]), (unsigned long long)(i + 1));
+  }
+}
+
+struct RowHi {  // row of a packed (lo << b | hi) key = lo
+  const unsigned long long* k;
+  int b;
+  __device__ int64_t operator()(int64_t i) const { return (int64_t)(k[i] >> b); }
+};
+struct RowU32 {
+  const uint32_t* k;
+  __device__ int64_t operator()(int64_t i) const { return (int64_t)k[i]; }
+};
+
+__global__ void k_eff_indices(const unsigned long long* __restrict__ keys, int64_t m, int b,
+                              int32_t* eff_indices, uint32_t* hi_out) {
+  unsigned long long mask = (1ull << b) - 1;
+  GRID_STRIDE(i, m) {
+    uint32_t hi = (uint32_t)(keys[i] & mask);
+    eff_indices[i] = (int32_t)hi;
+    hi_out[i] = hi;
+  }
+}
+
+__global__ void k_degrees(const int64_t* __restrict__ indptr, const int32_t* __restrict__ deg_orig,
+                          const int32_t* __restrict__ orig_ids, int64_t n, int32_t* deg,
+                          int32_t* eff_deg) {
+  GRID_STRIDE(v, n) {
+    eff_deg[v] = (int32_t)(indptr[v + 1] - indptr[v]);
+    deg[v] = deg_orig[orig_ids[v]];
+  }
+}
+
+__global__ void k_rev_fill(const int32_t* __restrict__ rev_e, const unsigned long long* __restrict__ keys,
+                           int b, const int64_t* __restrict__ eff_indptr, int64_t m,
+                           int32_t* rev_src, longlong2* rev_seg) {
+  GRID_STRIDE(j, m) {
+    int64_t e = rev_e[j];
+    int64_t v = (int64_t)(keys[e] >> b);
+    rev_src[j] = (int32_t)v;
+    rev_seg[j] = make_longlong2(e + 1, eff_indptr[v + 1]);
+  }
+}
+
+// Warp per u: pull-engine cost of u (see kSegCost / kTabCost).
+__global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const longlong2* __restrict__ rev_seg,
+                           const int64_t* __restrict__ eff_indptr, int64_t n, int64_t* cost) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    int64_t d = eff_indptr[u + 1] - eff_indptr[u];
+    int64_t r0 = rev_indptr[u], r1 = rev_indptr[u + 1];
+    long long s = 0;
+    if (d > 0)
+      for (int64_t r = r0 + lane; r < r1; r += 32) {
+        longlong2 sg = rev_seg[r];
+        s += (sg.y - sg.x) + kSegCost;
+      }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) cost[u] = (d > 0 && r1 > r0) ? (int64_t)s + d + kTabCost : 0;
+  }
+}
+
+// full CSR row u = predecessors (rev_src, ascending) then N^_u.
+__global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
+                       const int64_t* __restrict__ rev_indptr, const int32_t* __restrict__ rev_src,
+                       int64_t n, int64_t* full_indptr, int32_t* full_indices) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u <= n; u += nwarps) {
+    int64_t base = rev_indptr[u] + eff_indptr[u];
+    if (lane == 0) full_indptr[u] = base;
+    if (u == n) continue;
+    int64_t r0 = rev_indptr[u], r1 = rev_indptr[u + 1];
+    for (int64_t r = r0 + lane; r < r1; r += 32) full_indices[base + (r - r0)] = rev_src[r];
+    int64_t e0 = eff_indptr[u], e1 = eff_indptr[u + 1];
+    int64_t off = base + (r1 - r0);
+    for (int64_t e = e0 + lane; e < e1; e += 32) full_indices[off + (e - e0)] = eff_indices[e];
+  }
+}
+
+// ---------------------------------------------------------------- sorting
+
+template <class K>
+K* sort_keys(Scratch& sc, K* a, K* b, int64_t n, int end_bit, cudaStream_t s) {
+  if (n <= 1 || end_bit <= 0) return a;
+  cub::DoubleBuffer<K> db(a, b);
+  size_t tmp = 0;
+  TC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, n, 0, end_bit, s));
+  void* t = sc.bytes(tmp);
+  TC_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, n, 0, end_bit, s));
+  return db.Current();
+}
+
+template <class K, class V>
+void sort_pairs(Scratch& sc, K*& ka, K* kb, V*& va, V* vb, int64_t n, int end_bit,
+                cudaStream_t s) {
+  if (n <= 1 || end_bit <= 0) return;
+  cub::DoubleBuffer<K> dk(ka, kb);
+  cub::DoubleBuffer<V> dv(va, vb);
+  size_t tmp = 0;
+  TC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, n, 0, end_bit, s));
+  void* t = sc.bytes(tmp);
+  TC_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, n, 0, end_bit, s));
+  ka = dk.Current();
+  va = dv.Current();
+}
+
+
+template <class RowOf>
+void indptr_from_sorted(Scratch& sc, RowOf row_of, int64_t m, int64_t n, int64_t* indptr,
+                        cudaStream_t s) {
+  long long* cnt = sc.alloc<long long>(n + 1);
+  TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(long long), s));
+  if (m) {
+    k_row_counts<<<grid_for(m, kBlock, sm_count() * 16), kBlock, 0, s>>>(row_of, m, cnt);
+    check_launch();
+  }
+  size_t tmp = 0;
+  long long* out = reinterpret_cast<long long*>(indptr);
+  TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, out, n + 1, s));
+  void* t = sc.bytes(tmp);
+  TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cnt, out, n + 1, s));
+}
+
+template <class T>
+T read_scalar(const T* d, cudaStream_t s) {
+  T h;
+  TC_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);
+  return h;
+}
+
+// ---------------------------------------------------------------- normalize
+
+void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t* m_host,
+               int64_t* n_host, cudaStream_t s) {
+  *m_host = 0;
+  *n_host = 0;
+  TC_REQUIRE(m_raw >= 0, TC_EINVAL, "negative edge count");
+  TC_REQUIRE(m_raw < (1ll << 30), TC_EINVAL, "edge list too long for int32 positions (m_raw >= 2^30)");
+  if (m_raw == 0) return;
+  TC_REQUIRE(((uintptr_t)edges & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
+  Scratch sc(s);
+  int sms = sm_count();
+  int* mm = sc.alloc<int>(2);
+  int init[2] = {INT_MAX, INT_MIN};
+  TC_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  k_minmax<<<grid_for(2 * m_raw, kBlock, sms * 8), kBlock, 0, s>>>(edges, 2 * m_raw, mm, mm + 1);
+  check_launch();
+  int hmm[2];
+  TC_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);
+  TC_REQUIRE(hmm[0] >= 0, TC_EINVAL, "negative node id in edge list");  // graph.py:87-88
+
+  // drop self-loops (graph.py:89)
+  auto* e1 = sc.alloc<unsigned long long>(m_raw);
+  auto* nsel = sc.alloc<long long>(1);
+  {
+    size_t tmp = 0;
+    auto in = reinterpret_cast<const unsigned long long*>(edges);
+    TC_CUDA(cub::DeviceSelect::If(nullptr, tmp, in, e1, nsel, m_raw, NotSelfLoop(), s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceSelect::If(t, tmp, in, e1, nsel, m_raw, NotSelfLoop(), s));
+  }
+  int64_t m1 = read_scalar(nsel, s);
+  if (m1 == 0) return;  // graph.py:90-91
+  int32_t* ids = reinterpret_cast<int32_t*>(e1);
+  int64_t nid = 2 * m1;
+  int64_t L1 = (int64_t)hmm[1] + 1;
+
+  // first occurrence of each label in the raveled order (graph.py:92-93)
+  uint32_t* fp = sc.alloc<uint32_t>(L1);
+  TC_CUDA(cudaMemsetAsync(fp, 0xFF, L1 * sizeof(uint32_t), s));
+  k_first_pos<<<grid_for(nid, kBlock, sms * 16), kBlock, 0, s>>>(ids, nid, fp);
+  check_launch();
+  auto* cnt = sc.alloc<unsigned long long>(1);
+  int* lf = sc.alloc<int>(1);
+  TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+  int minus1 = -1;
+  TC_CUDA(cudaMemcpyAsync(lf, &minus1, sizeof(int), cudaMemcpyHostToDevice, s));
+  k_present<<<grid_for(L1, kBlock, sms * 8), kBlock, 0, s>>>(fp, L1, cnt, lf);
+  check_launch();
+  int64_t K = (int64_t)read_scalar(cnt, s);
+  int64_t Lf = read_scalar(lf, s);
+
+  if (K != Lf + 1) {
+    // first-seen compaction (graph.py:96-98): new id = rank of first position
+    int32_t* pid = sc.alloc<int32_t>(K);
+    int32_t* pid2 = sc.alloc<int32_t>(K);
+    {
+      size_t tmp = 0;
+      cub::CountingInputIterator<int> it(0);
+      IsPresent pred{fp};
+      TC_CUDA(cub::DeviceSelect::If(nullptr, tmp, it, pid, nsel, L1, pred, s));
+      void* t = sc.bytes(tmp);
+      TC_CUDA(cub::DeviceSelect::If(t, tmp, it, pid, nsel, L1, pred, s));
+    }
+    uint32_t* fk = sc.alloc<uint32_t>(K);
+    uint32_t* fk2 = sc.alloc<uint32_t>(K);
+    k_gather_u32<<<grid_for(K, kBlock), kBlock, 0, s>>>(pid, fp, K, fk);
+    check_launch();
+    sort_pairs(sc, fk, fk2, pid, pid2, K, bits_for((uint64_t)nid), s);
+    int32_t* new_id = reinterpret_cast<int32_t*>(fp);  // fp no longer needed
+    k_rank_scatter<<<grid_for(K, kBlock), kBlock, 0, s>>>(pid, K, new_id);
+    check_launch();
+    k_remap<<<grid_for(nid, kBlock, sms * 16), kBlock, 0, s>>>(ids, nid, new_id);
+    check_launch();
+  }
+
+  // (lo, hi) + unique rows (graph.py:99-102)
+  int b = std::max(1, bits_for((uint64_t)(K - 1)));
+  auto* ka = sc.alloc<unsigned long long>(m1);
+  auto* kb = sc.alloc<unsigned long long>(m1);
+  k_pack_pairs<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, nullptr, b, ka);
+  check_launch();
+  unsigned long long* sorted = sort_keys(sc, ka, kb, m1, 2 * b, s);
+  unsigned long long* uniq = (sorted == ka) ? kb : ka;
+  {
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel, m1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, uniq, nsel, m1, s));
+  }
+  int64_t m2 = read_scalar(nsel, s);
+  k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, b, out_edges);
+  check_launch();
+  sync_stream(s);
+  *m_host = m2;
+  *n_host = K;  // graph.py:103
+}
+
+// ---------------------------------------------------------------- build
+
+void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
+                 int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel, int32_t* orig_ids,
+                 int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr, int32_t* rev_src,
+                 int64_t* rev_seg, int64_t* rev_cost, cudaStream_t s) {
+  TC_REQUIRE(n >= 0 && m >= 0, TC_EINVAL, "negative size");
+  TC_REQUIRE(n < (1ll << 31) - 1, TC_EINVAL, "n must fit int32 ids");
+  TC_REQUIRE(m < (1ll << 31) - 1, TC_EINVAL, "m must be < 2^31");
+  Scratch sc(s);
+  int sms = sm_count();
+  if (m > 0) {
+    int* bad = sc.alloc<int>(1);
+    TC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    k_range_check<<<grid_for(2 * m, kBlock, sms * 8), kBlock, 0, s>>>(edges, 2 * m, n, bad);
+    check_launch();
+    int hb = read_scalar(bad, s);
+    TC_REQUIRE(!(hb & 1), TC_EINVAL, "negative node id in edge list");
+    TC_REQUIRE(!(hb & 2), TC_EINDEX, "edge endpoint >= n");
+  }
+  if (n == 0) {
+    TC_CUDA(cudaMemsetAsync(eff_indptr, 0, sizeof(int64_t), s));
+    TC_CUDA(cudaMemsetAsync(rev_indptr, 0, sizeof(int64_t), s));
+    TC_CUDA(cudaMemsetAsync(rev_cost, 0, sizeof(int64_t), s));
+    return;
+  }
+  // degrees (graph.py:149-151)
+  int32_t* deg_orig = sc.alloc<int32_t>(n);
+  TC_CUDA(cudaMemsetAsync(deg_orig, 0, n * sizeof(int32_t), s));
+  if (m) {
+    k_histogram<<<grid_for(2 * m, kBlock, sms * 16), kBlock, 0, s>>>(edges, 2 * m, deg_orig);
+    check_launch();
+  }
+  // canonical order: ascending (degree, id) via a stable radix sort (graph.py:152)
+  if (order) {
+    k_copy_i32<<<grid_for(n, kBlock), kBlock, 0, s>>>(order, orig_ids, n);
+    check_launch();
+  } else {
+    uint32_t* dk = sc.alloc<uint32_t>(n);
+    uint32_t* dk2 = sc.alloc<uint32_t>(n);
+    int32_t* ov = sc.alloc<int32_t>(n);
+    int32_t* ov2 = sc.alloc<int32_t>(n);
+    TC_CUDA(cudaMemcpyAsync(dk, deg_orig, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    k_iota<<<grid_for(n, kBlock), kBlock, 0, s>>>(ov, n);
+    check_launch();
+    sort_pairs(sc, dk, dk2, ov, ov2, n, std::max(1, bits_for((uint64_t)(2 * m))), s);
+    TC_CUDA(cudaMemcpyAsync(orig_ids, ov, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  }
+  k_rank_scatter<<<grid_for(n, kBlock), kBlock, 0, s>>>(orig_ids, n, relabel);  // graph.py:111-112
+  check_launch();
+
+  // orientation + forward CSR (graph.py:113-124)
+  int b = std::max(1, bits_for((uint64_t)(n - 1)));
+  auto* ka = sc.alloc<unsigned long long>(m);
+  auto* kb = sc.alloc<unsigned long long>(m);
+  if (m) {
+    k_pack_pairs<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, b, ka);
+    check_launch();
+  }
+  unsigned long long* keys = sort_keys(sc, ka, kb, m, 2 * b, s);
+  indptr_from_sorted(sc, RowHi{keys, b}, m, n, eff_indptr, s);
+  uint32_t* hi = sc.alloc<uint32_t>(m);
+  uint32_t* hi2 = sc.alloc<uint32_t>(m);
+  if (m) {
+    k_eff_indices<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indices, hi);
+    check_launch();
+  }
+  k_degrees<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, deg_orig, orig_ids, n, deg, eff_deg);
+  check_launch();
+
+  // reverse CSR: predecessors of u sorted by v (stable sort by hi of the
+  // lo-sorted edge list), each with the suffix of N^_v after u.
+  int32_t* re = sc.alloc<int32_t>(m);
+  int32_t* re2 = sc.alloc<int32_t>(m);
+  if (m) {
+    k_iota<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(re, m);
+    check_launch();
+  }
+  sort_pairs(sc, hi, hi2, re, re2, m, b, s);
+  indptr_from_sorted(sc, RowU32{hi}, m, n, rev_indptr, s);
+  if (m) {
+    k_rev_fill<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(re, keys, b, eff_indptr, m, rev_src,
+                                                                reinterpret_cast<longlong2*>(rev_seg));
+    check_launch();
+  }
+  // pull-engine cost prefix over u
+  int64_t* cu = sc.alloc<int64_t>(n + 1);
+  k_rev_cost<<<grid_for(n * 32, kBlock, sms * 16), kBlock, 0, s>>>(
+      rev_indptr, reinterpret_cast<const longlong2*>(rev_seg), eff_indptr, n, cu);
+  check_launch();
+  TC_CUDA(cudaMemsetAsync(cu + n, 0, sizeof(int64_t), s));
+  {
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cu, rev_cost, n + 1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cu, rev_cost, n + 1, s));
+  }
+}
+
+// ---------------------------------------------------------------- costs
+
+__global__ void k_cost_simple(int kind, const int32_t* __restrict__ deg, int64_t n, int64_t* out) {
+  GRID_STRIDE(v, n) out[v] = (kind == TC_COST_UNIT) ? 1 : (kind == TC_COST_DEGREE ? (int64_t)deg[v] : 0);
+}
+
+// SUCC_SUM (partitioning.py:89): warp per v, sum over N^_v of d^_v + d^_u.
+__global__ void k_cost_succ(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int32_t* __restrict__ eff_deg, int64_t n, int64_t* out) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    int64_t e0 = indptr[v], e1 = indptr[v + 1];
+    long long s = 0;
+    for (int64_t e = e0 + lane; e < e1; e += 32) s += eff_deg[indices[e]];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[v] = (int64_t)s + (e1 - e0) * (e1 - e0);
+  }
+}
+
+// PRED_SUM (partitioning.py:91): each edge (v,u) adds d^_v + d^_u to u.
+__global__ void k_cost_pred(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int32_t* __restrict__ eff_deg, int64_t n, int64_t* out) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    int64_t e0 = indptr[v], e1 = indptr[v + 1];
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      int32_t u = indices[e];
+      atomicAdd(reinterpret_cast<unsigned long long*>(&out[u]),
+                (unsigned long long)((e1 - e0) + eff_deg[u]));
+    }
+  }
+}
+
+void node_costs(int kind, const int64_t* eff_indptr, const int32_t* eff_indices, const int32_t* deg,
+                const int32_t* eff_deg, int64_t n, int64_t* out, cudaStream_t s) {
+  TC_REQUIRE(kind >= 0 && kind <= 3, TC_EINVAL, "unknown cost kind");
+  if (n == 0) return;
+  int sms = sm_count();
+  k_cost_simple<<<grid_for(n, kBlock), kBlock, 0, s>>>(kind, deg, n, out);
+  check_launch();
+  if (kind == TC_COST_SUCC_SUM) {
+    k_cost_succ<<<grid_for(n * 32, kBlock, sms * 16), kBlock, 0, s>>>(eff_indptr, eff_indices, eff_deg, n, out);
+  } else if (kind == TC_COST_PRED_SUM) {
+    k_cost_pred<<<grid_for(n * 32, kBlock, sms * 16), kBlock, 0, s>>>(eff_indptr, eff_indices, eff_deg, n, out);
+  }
+  check_launch();
+}
+
+}  // namespace tcb
+
+extern "C" {
+
+int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t* m_host,
+                 int64_t* n_host, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    tcb::normalize(edges, m_raw, out_edges, m_host, n_host, (cudaStream_t)stream);
+  });
+}
+
+int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
+                   int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
+                   int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
+                   int32_t* rev_src, int64_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    tcb::build_graph(edges, m, n, order, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
+                     rev_indptr, rev_src, rev_seg, rev_cost, (cudaStream_t)stream);
+  });
+}
+
+int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
+                  const int64_t* rev_indptr, const int32_t* rev_src, int64_t n,
+                  int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    int sms = tcb::sm_count();
+    tcb::k_full<<<tcb::grid_for((n + 1) * 32, 256, sms * 16), 256, 0, s>>>(
+        eff_indptr, eff_indices, rev_indptr, rev_src, n, full_indptr, full_indices);
+    tcb::check_launch();
+  });
+}
+
+int tc_node_costs(int32_t kind, const int64_t* eff_indptr, const int32_t* eff_indices,
+                  const int32_t* deg, const int32_t* eff_deg, int64_t n, int64_t* out,
+                  tc_stream_t stream) {
+  return tcb::guarded([&] {
+    tcb::node_costs(kind, eff_indptr, eff_indices, deg, eff_deg, n, out, (cudaStream_t)stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// common.cuh -- shared helpers for libtcb200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tcb200.h"
+
+namespace tcb {
+
+// Error carried from the implementation to the C-ABI boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define TC_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e__ = (call);                                                      \
+    if (e__ != cudaSuccess)                                                        \
+      throw ::tcb::Error(TC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define TC_REQUIRE(cond, code, msg)                       \
+  do {                                                    \
+    if (!(cond)) throw ::tcb::Error((code), (msg));       \
+  } while (0)
+
+// Runs `body` and maps exceptions to C-ABI status codes.
+template <class F>
+int guarded(F&& body) {
+  try {
+    body();
+    return TC_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return TC_ENOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TC_ECUDA;
+  }
+}
+
+// Stream-ordered scratch memory (cudaMallocAsync from the device pool);
+// everything is released on the same stream when the guard dies, so the
+// library never holds device memory across calls.
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t s) : s_(s) {}
+  ~Scratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, s_);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    size_t bytes = (n ? n : 1) * sizeof(T);
+    cudaError_t e = cudaMallocAsync(&p, bytes, s_);
+    if (e != cudaSuccess)
+      throw Error(TC_ENOMEM, std::string("cudaMallocAsync(") + std::to_string(bytes) +
+                                 "): " + cudaGetErrorString(e));
+    ptrs_.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void* bytes(size_t n) { return alloc<unsigned char>(n); }
+
+ private:
+  cudaStream_t s_;
+  std::vector<void*> ptrs_;
+};
+
+inline int bits_for(uint64_t v) {
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+inline int grid_for(int64_t n, int block, int max_blocks = 148 * 32) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+int sm_count();
+
+inline void sync_stream(cudaStream_t s) { TC_CUDA(cudaStreamSynchronize(s)); }
+
+inline void check_launch() { TC_CUDA(cudaGetLastError()); }
+
+}  // namespace tcb
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)

@@ -1,0 +1,300 @@
+"""GPU parity: every entry point through the C ABI against the reference's
+own outputs (tests/golden, produced by running /root/reference) and, for
+inputs without fixtures, against the CPU oracle (oracle/, itself pinned to
+the reference by test_oracle_golden.py).  Integer work: bit-exact."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import SMALL, SMALL_NAMES
+import paper_1406_5687_b200 as tcb
+from paper_1406_5687_b200 import graph as G
+from paper_1406_5687_b200.graph_io import er_edges, pa_edges_host, rmat_edges
+from paper_1406_5687_b200.sequential import count_lowest, count_middle
+from oracle import gen_twin
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KINDS = {"unit": tcb.CostKind.UNIT, "degree": tcb.CostKind.DEGREE,
+         "succsum": tcb.CostKind.SUCC_SUM, "predsum": tcb.CostKind.PRED_SUM}
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.int64)
+
+
+_GRAPHS = {}
+
+
+def graph_of(name):
+    if name not in _GRAPHS:
+        case = SMALL[name]
+        raw = tcb.RawGraph.from_pairs(case["raw"])
+        norm = tcb.normalize(raw)
+        _GRAPHS[name] = (norm, tcb.build_graph(norm))
+    return _GRAPHS[name]
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_normalize_parity(name):
+    case = SMALL[name]
+    norm, _ = graph_of(name)
+    assert norm.n == int(case["norm_n"][0])
+    assert np.array_equal(host(norm.edges).reshape(-1, 2), case["norm_edges"].reshape(-1, 2))
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_build_parity(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    for f in ("eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg",
+              "full_indptr", "full_indices"):
+        assert np.array_equal(host(getattr(g, f)), case[f]), f
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_count_parity(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    T = int(case["T"][0])
+    assert tcb.count_triangles_seq(g) == T
+    if g.n:
+        assert int(count_lowest(g).item()) == T  # the second engine agrees
+    if g.n <= 2000:
+        assert tcb.count_triangles_brute(g) == T
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_costs_and_ranges_parity(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    for kname, kind in KINDS.items():
+        assert np.array_equal(host(tcb.node_costs(g, kind)), case[f"cost_{kname}"]), kname
+    if g.n == 0:
+        return
+    for P in (2, 3, 5, 8):
+        for kname in ("predsum", "succsum", "degree"):
+            b = tcb.range_bounds(tcb.partition_ranges(g, KINDS[kname], P))
+            assert np.array_equal(b, case[f"bounds_{kname}_{P}"]), (kname, P)
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_surrogate_parity(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    if g.n == 0:
+        return
+    for P in (2, 3, 5, 8):
+        total, rr = tcb.count_space_surrogate(g, P)
+        assert total == int(case["T"][0])
+        assert [m.triangles for m in rr.metrics] == case[f"surr_tri_{P}"].tolist()
+        assert np.array_equal(np.stack([m.data_msgs_to for m in rr.metrics]), case[f"surr_census_{P}"])
+        assert [m.data_msgs_sent for m in rr.metrics] == case[f"surr_msgs_{P}"].tolist()
+        assert [m.bytes_sent for m in rr.metrics] == case[f"surr_bytes_{P}"].tolist()
+        assert [m.partition_bytes for m in rr.metrics] == case[f"surr_pbytes_{P}"].tolist()
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_lowest_vertex_partials_and_plan(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    if g.n == 0:
+        return
+    for P in (2, 3, 5, 8):
+        bounds = case[f"bounds_predsum_{P}"]
+        got = [tcb.count_task(g, tcb.Task(int(bounds[i]), int(bounds[i + 1] - bounds[i])))
+               if bounds[i + 1] > bounds[i] else 0 for i in range(P)]
+        assert got == case[f"lowest_{P}"].tolist()
+        binned = host(count_lowest(g, 0, g.n, bounds=torch.as_tensor(bounds).cuda()))
+        assert binned.tolist() == case[f"lowest_{P}"].tolist()
+        plan = tcb.plan_tasks(tcb.node_costs(g, tcb.CostKind.DEGREE), P + 1)
+        assert plan.split == int(case[f"plan_split_{P}"][0])
+        assert np.array_equal(tcb.range_bounds(plan.initial), case[f"plan_initial_{P}"])
+        q = np.array([(t.v, t.t) for t in plan.queue], np.int64).reshape(-1, 2)
+        assert np.array_equal(q, case[f"plan_queue_{P}"].reshape(-1, 2))
+        assert np.allclose(plan.targets, case[f"plan_targets_{P}"])
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_count_dynamic_accounting(name):
+    case = SMALL[name]
+    _, g = graph_of(name)
+    T = int(case["T"][0])
+    for nranks in (2, 4, 9):
+        total, rr = tcb.count_dynamic(g, nranks)
+        assert total == T
+        assert rr.metrics[0].tasks_executed == 0 and rr.metrics[0].triangles == 0
+        covered = sorted(v for m in rr.metrics[1:] for (s, t) in m.task_log for v in range(s, s + t))
+        assert covered == list(range(g.n))
+        assert sum(m.triangles for m in rr.metrics) == total
+    total, rr = tcb.count_dynamic(g, 5, static_only=True)
+    assert total == T
+    assert all(m.requests_sent == 1 for m in rr.metrics[1:])
+
+
+def test_known_answers(known):
+    def gp(pairs, n=None):
+        return tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(pairs, n=n)))
+
+    def comp(n):
+        return gp([(a, b) for a in range(n) for b in range(a + 1, n)])
+
+    assert tcb.count_triangles_seq(comp(3)) == known["K3"]
+    assert tcb.count_triangles_seq(comp(4)) == known["K4"]
+    assert tcb.count_triangles_seq(comp(9)) == known["K9"]
+    assert tcb.count_triangles_seq(gp([(0, 1), (1, 2)])) == known["path"]
+    k3 = comp(3)
+    assert [host(k3.succ(v)).tolist() for v in range(3)] == known["k3_succ"]
+    assert host(gp([(0, 1), (0, 2), (1, 3)]).relabel).tolist() == known["tie_break_relabel"]
+    assert int(gp([(0, 1), (0, 2), (0, 3)]).relabel[0]) == known["star_relabel0"]
+    pa = tcb.build_graph(tcb.normalize(tcb.generate_pa(tcb.PaParams(10_000, 20, 1))))
+    assert pa.m == known["PA_10000_20_1_m"]
+    assert int(pa.deg.max()) == known["PA_10000_20_1_maxdeg"]
+    assert tcb.count_triangles_seq(pa) == known["PA_10000_20_1_T"]
+    for kind, vals in known["costs_K3"].items():
+        assert host(tcb.node_costs(k3, tcb.CostKind(kind))).tolist() == vals
+    for r in known["ranges"]:
+        got = tcb.balanced_ranges(r["costs"], tcb.NodeRange(0, len(r["costs"])), r["k"])
+        assert [[x.start, x.count] for x in got] == r["out"]
+    plan = tcb.plan_tasks(np.ones(100, dtype=np.int64), 5)
+    assert plan.split == known["plan_unit_100_5"]["split"]
+    assert [r.count for r in plan.initial] == known["plan_unit_100_5"]["initial"]
+    assert [t.t for t in plan.queue] == known["plan_unit_100_5"]["queue"]
+    assert [tcb.surrogate_count(x, c, k3) for x, c in
+            [([], tcb.NodeRange(0, 3)), (k3.succ(0), tcb.NodeRange(2, 1)),
+             (k3.succ(0), tcb.NodeRange(1, 1))]] == known["surrogate_count_k3"]
+
+
+def test_edge_cases():
+    empty = tcb.normalize(tcb.RawGraph.from_pairs([]))
+    assert empty.n == 0 and tuple(empty.edges.shape) == (0, 2)
+    g = tcb.build_graph(empty)
+    assert g.n == 0 and g.m == 0 and tcb.count_triangles_seq(g) == 0
+    loops = tcb.normalize(tcb.RawGraph.from_pairs([(3, 3), (5, 5)]))
+    assert loops.n == 0
+    iso = tcb.build_graph(tcb.RawGraph(n=5, edges=np.array([[3, 4]], dtype=np.int64)))
+    assert iso.n == 5 and int(iso.deg.sum()) == 2 and tcb.count_triangles_seq(iso) == 0
+    assert int(iso.deg[0]) == 0 and int(iso.deg[2]) == 0
+    with pytest.raises(ValueError):
+        tcb.normalize(tcb.RawGraph(n=2, edges=np.array([[-1, 0]])))
+    with pytest.raises(IndexError):
+        tcb.build_graph(tcb.RawGraph(n=2, edges=np.array([[0, 5]])))
+    with pytest.raises(AssertionError):
+        tcb.intersect_count([2, 1], [1, 2])
+    assert tcb.intersect_count([1, 2, 5], [2, 5, 9]) == 2
+    assert tcb.intersect_count([], [1, 2]) == 0
+    k4 = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs([(a, b) for a in range(4) for b in range(a + 1, 4)])))
+    assert tcb.count_task(k4, tcb.Task(0, 4)) == 4
+    assert tcb.count_task(k4, tcb.Task(3, 1)) == 0
+    with pytest.raises(ValueError):
+        tcb.count_task(k4, tcb.Task(2, 5))
+    with pytest.raises(ValueError):
+        tcb.plan_tasks([1, 2, 3], 1)
+    with pytest.raises(ValueError):
+        tcb.plan_tasks([1, -2, 3], 3)
+    with pytest.raises(IndexError):
+        k4.precedes(0, 9)
+    big = tcb.build_graph(tcb.RawGraph(n=2500, edges=np.array([[0, 1]])))
+    with pytest.raises(ValueError):
+        tcb.count_triangles_brute(big)
+    tri = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs([(0, 1), (1, 2), (0, 2)])))
+    total, _ = tcb.count_dynamic(tri, 9)
+    assert total == 1
+
+
+def test_input_order_hook_counts_match():
+    for seed in range(3):
+        raw = tcb.normalize(tcb.RawGraph.from_pairs(gen_twin.er_gnm(60, 400, seed)))
+        g = tcb.build_graph(raw)
+        alt = G._build_graph_input_order(raw)
+        assert tcb.count_triangles_seq(alt) == tcb.count_triangles_seq(g)
+        assert np.array_equal(host(alt.relabel), np.arange(raw.n))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_device_generators_match_twin_and_oracle(seed):
+    e = er_edges(3000, 40000, seed)
+    assert np.array_equal(host(e), gen_twin.er_gnm(3000, 40000, seed).astype(np.int64))
+    r = rmat_edges(11, 8, seed)
+    assert np.array_equal(host(r), gen_twin.rmat(11, 8, seed).astype(np.int64))
+    for raw in (e, r):
+        og = O.build_graph(*O.normalize(host(raw)))
+        g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw)))
+        assert np.array_equal(host(g.eff_indices), og.eff_indices)
+        assert np.array_equal(host(g.relabel), og.relabel)
+        T = O.count_triangles(og)
+        assert tcb.count_triangles_seq(g) == T
+        b = O.balanced_bounds(O.node_costs(og, "predsum"), 0, og.n, 4)
+        partials, census = O.surrogate(og, b)
+        total, rr = tcb.count_space_surrogate(g, 4)
+        assert [m.triangles for m in rr.metrics] == partials.tolist()
+        assert np.array_equal(np.stack([m.data_msgs_to for m in rr.metrics]), census)
+
+
+def test_cfg1_instance(configs):
+    c = configs["cfg1_er_gnm_16384_131072_seed1"]
+    raw = er_edges(16384, 131072, 1)
+    assert gen_twin.checksum(host(raw)) == c["raw_checksum"]
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=16384, edges=raw)))
+    assert (g.n, g.m) == (c["n"], c["m"])
+    assert gen_twin.checksum(host(g.eff_indices)) == c["eff_indices_checksum"]
+    assert gen_twin.checksum(host(g.eff_indptr)) == c["eff_indptr_checksum"]
+    assert gen_twin.checksum(host(g.relabel)) == c["relabel_checksum"]
+    assert tcb.count_triangles_seq(g) == c["T"]
+    assert int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum()) == c["W"]
+    for P in (2, 4, 8):
+        total, rr = tcb.count_space_surrogate(g, P)
+        assert [m.triangles for m in rr.metrics] == c[f"surr_tri_{P}"]
+        assert np.stack([m.data_msgs_to for m in rr.metrics]).tolist() == c[f"surr_census_{P}"]
+        b = torch.as_tensor(np.array(c[f"bounds_predsum_{P}"])).cuda()
+        assert host(count_lowest(g, 0, g.n, bounds=b)).tolist() == c[f"lowest_{P}"]
+
+
+def test_cfg2_full_scale(configs):
+    key = "cfg2_pa_1000000_100_seed1"
+    if key not in configs:
+        pytest.skip("cfg2 golden not generated (make_golden.py --big)")
+    c = configs[key]
+    raw = pa_edges_host(tcb.PaParams(1_000_000, 100, 1))
+    assert gen_twin.checksum(raw.numpy()) == c["raw_checksum"]
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=1_000_000, edges=raw)))
+    assert (g.n, g.m) == (c["n"], c["m"])
+    assert gen_twin.checksum(host(g.eff_indices)) == c["eff_indices_checksum"]
+    assert tcb.count_triangles_seq(g) == c["T"]
+    assert int(count_lowest(g).item()) == c["T"]
+    assert int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum()) == c["W"]
+    for P in (2, 4, 8):
+        total, rr = tcb.count_space_surrogate(g, P)
+        assert total == c["T"]
+        assert [m.triangles for m in rr.metrics] == c[f"surr_tri_{P}"]
+        assert np.stack([m.data_msgs_to for m in rr.metrics]).tolist() == c[f"surr_census_{P}"]
+
+
+def test_rmat_scale_properties():
+    """Size-independent properties at a scale the oracle would take minutes
+    on: both engines agree, partials tile the total, repeat runs are
+    identical, and the identity ordering gives the same count."""
+    raw = rmat_edges(18, 16, 3)
+    norm = tcb.normalize(tcb.RawGraph(n=1 << 18, edges=raw))
+    g = tcb.build_graph(norm)
+    T = tcb.count_triangles_seq(g)
+    assert T > 0
+    assert int(count_lowest(g).item()) == T
+    assert tcb.count_triangles_seq(g) == T
+    for P in (3, 8):
+        total, rr = tcb.count_space_surrogate(g, P)
+        assert total == T
+        b = torch.as_tensor(tcb.range_bounds(tcb.partition_ranges(g, tcb.CostKind.SUCC_SUM, P))).cuda()
+        assert int(count_lowest(g, 0, g.n, bounds=b).sum()) == T
+        assert int(count_middle(g, 0, g.n, bounds=b).sum()) == T
+    alt = G._build_graph_input_order(norm)
+    assert tcb.count_triangles_seq(alt) == T
+    # structure invariants: orientation partitions E, rows strictly ascending
+    ip, ix = host(g.eff_indptr), host(g.eff_indices)
+    src = np.repeat(np.arange(g.n), np.diff(ip))
+    assert np.all(ix > src)
+    same_row = src[1:] == src[:-1]
+    assert np.all(ix[1:][same_row] > ix[:-1][same_row])
+    assert int(g.deg.sum()) == 2 * g.m
