@@ -98,6 +98,30 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
                     int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, tc_stream_t stream);
 
+/* Generic engine over k "virtual owners": owner x probes the table list
+ * N^_{owner_map[x]} (owner_map NULL: identity) with segments
+ * segs[row_indptr[x] .. row_indptr[x+1]) (pairs into `pool`); cost_prefix
+ * int64[k+1] drives the chunk plan.  mode 0 = the paper's schedule (half
+ * the cost in one chunk per warp, then geometric), mode 1 = owner-ordered
+ * uniform chunks then a geometric tail (for L2-tiled owners).  Buckets bin
+ * owner_map[x].  out is overwritten. */
+int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
+                    const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                    const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int32_t nbuckets,
+                    unsigned long long* out, int32_t mode, tc_stream_t stream);
+
+/* L2-tiled regrouping of the predecessor entries of u in [u0, u1): v is cut
+ * into tiles of <= tile_ids list entries and entries are ordered
+ * (tile(v), u, v); each (tile, u) with entries is one virtual owner.
+ * Outputs (capacity E = rev_indptr[u1] - rev_indptr[u0]): owner_u int32[E],
+ * owner_ptr int64[E+1], segs int64[2E], cost_prefix int64[E+1]; returns the
+ * owner count k and the tile count.  Feed to tc_count_owners (mode 1).
+ * Synchronises. */
+int tc_tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
+                 const int32_t* rev_src, const int64_t* rev_seg, int64_t u0, int64_t u1,
+                 int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int64_t* segs,
+                 int64_t* cost_prefix, int64_t* k_host, int64_t* ntiles_host, tc_stream_t stream);
+
 /* Lowest-vertex ("push") engine: count_node_range(v0, v1)
  * (_kernels.py:40-52) with per-bucket partials: out[b] = triangles whose
  * lowest vertex lies in [bucket_bounds[b], bucket_bounds[b+1]).

@@ -13,7 +13,7 @@ import subprocess
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libtcb200.so")
+_SO = os.environ.get("TCB_LIB") or os.path.join(_HERE, "libtcb200.so")
 _LIB = None
 
 TC_OK, TC_EINVAL, TC_EINDEX, TC_ECUDA, TC_ENOMEM = 0, -1, -2, -3, -4
@@ -30,6 +30,8 @@ _SIGS = {
     "tc_build_full": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
+    "tc_count_owners": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp],
+    "tc_tile_pull": [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "tc_intersect_count": [_vp, _i64, _vp, _i64, _vp, _vp],
     "tc_engine_timing": [_i32, _vp, _vp],
     "tc_count_brute": [_vp, _vp, _i64, _vp, _vp],

@@ -34,10 +34,17 @@
 
 namespace tcb {
 
+#ifndef TCB_MINBLOCKS
+#define TCB_MINBLOCKS 6
+#endif
+#ifndef TCB_WINDOWS
+#define TCB_WINDOWS 2
+#endif
 static constexpr int kWarps = 8;          // warps per block
+static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
 static constexpr int kTabCap = 256;       // sorted-table capacity per warp (elements)
-static constexpr int kBmWords = 256;      // bitmap words per warp (8192 bits)
+static constexpr int kBmWords = 512;      // filter words per warp (16384 bits)
 static constexpr int kSegCost = 2;        // must match build.cu
 static constexpr int kTabCost = 16;
 
@@ -102,6 +109,7 @@ struct EngineArgs {
   int nbuckets;
   unsigned long long* out;
   int64_t n_owner;            // row_indptr has n_owner + 1 entries
+  const int32_t* owner_map;   // nullable: owner x -> table/bucket node id
 };
 
 __device__ __forceinline__ int bucket_of(const int64_t* bb, int nb, int64_t x) {
@@ -115,8 +123,97 @@ __device__ __forceinline__ int bucket_of(const int64_t* bb, int nb, int64_t x) {
   return lo;
 }
 
+// Hashed one-bit filter over one owner's list: bit (h >> 18) of the 16K-bit
+// word array (word h >> 23, bit (h >> 18) & 31), h = w * golden.  A probe is
+// one LDS and three ALU ops; the false-positive rate is d / 16384 per probe,
+// and positives are verified by binary search in the sorted copy.
+__device__ __forceinline__ uint32_t filt_hash(uint32_t w) { return w * 0x9E3779B1u; }
+
+__device__ __forceinline__ void filt_insert(uint32_t* bm, int32_t w) {
+  uint32_t h = filt_hash((uint32_t)w);
+  atomicOr(&bm[h >> 23], 1u << ((h >> 18) & 31));
+}
+
+// 4-bit mask of the elements of v (valid ones per vmask) that pass the
+// range check and hit the filter.  Branch-free.
+__device__ __forceinline__ uint32_t filt_probe4(const uint32_t* bm, int4 v, uint32_t vmask, int32_t tmin,
+                                                int32_t tmax) {
+  uint32_t m = 0;
+  int32_t xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t h = filt_hash((uint32_t)xs[k]);
+    uint32_t wd = bm[h >> 23];
+    uint32_t bit = (wd >> ((h >> 18) & 31)) & 1u;
+    bool in = ((vmask >> k) & 1u) && xs[k] >= tmin && xs[k] <= tmax;
+    m |= (in ? bit : 0u) << k;
+  }
+  return m;
+}
+
+// Resolve the probes of one group of <= 32 compacted segments.  The group is
+// flattened over the 16-byte chunks its segments touch: lane j of window k
+// loads chunk base+32k+j as one int4 (4 list elements) and probes the
+// elements of it that lie inside its segment.  Two windows are in flight.
+// Segment s covers chunks [excl_s, endx_s) of the flat space; chunk f of it
+// is pool4[delta_s + f]; `edge_s` packs (first-chunk offset | last-chunk
+// count << 2).
+template <bool kSmall>
+__device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const WarpSlice& sl,
+                                            const int32_t* __restrict__ gtab, int64_t d, int32_t tmin,
+                                            int32_t tmax, int nseg, int excl, int endx, int edge,
+                                            int64_t delta, int total, int lane, uint32_t& cnt) {
+  const unsigned FULL = 0xffffffffu;
+  const bool lane_seg = lane < nseg;
+  for (int base = 0; base < total; base += 32 * kWin) {
+    int4 v[kWin];
+    uint32_t vm[kWin];
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) {
+      const int b = base + 32 * k;
+      vm[k] = 0;
+      v[k] = make_int4(0, 0, 0, 0);
+      if (b < total) {
+        unsigned cov = __ballot_sync(FULL, lane_seg && excl <= b);
+        int c0 = __popc(cov) - 1;
+        unsigned bit = (lane_seg && excl > b && excl < b + 32) ? (1u << (excl - b)) : 0u;
+        unsigned starts = __reduce_or_sync(FULL, bit);
+        int sj = c0 + __popc(starts & ((2u << lane) - 1u));
+        int64_t dl = __shfl_sync(FULL, delta, sj);
+        int ex = __shfl_sync(FULL, excl, sj);
+        int en = __shfl_sync(FULL, endx, sj);
+        int eg = __shfl_sync(FULL, edge, sj);
+        int f = b + lane;
+        if (f < total) {
+          v[k] = __ldg(&pool4[dl + f]);
+          uint32_t lo = (f == ex) ? (uint32_t)(eg & 3) : 0u;
+          uint32_t hi = (f == en - 1) ? (uint32_t)(eg >> 2) : 4u;
+          vm[k] = (0xFu >> (4 - hi)) & (0xFu << lo);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kWin; ++k) {
+      if (kSmall) {
+        uint32_t m = filt_probe4(sl.bm, v[k], vm[k], tmin, tmax);
+        if (m) {
+          int32_t xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((m >> e) & 1u) cnt += bsearch_smem(sl.tab, (int)d, xs[e]);
+        }
+      } else {
+        int32_t xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (((vm[k] >> e) & 1u) && xs[e] >= tmin && xs[e] <= tmax) cnt += bsearch_gmem(gtab, d, xs[e]);
+      }
+    }
+  }
+}
+
 template <class Segs>
-__global__ void __launch_bounds__(kThreads) k_engine(EngineArgs a, Segs segs) {
+__global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSlice slices[kWarps];
   const int lane = threadIdx.x & 31;
   WarpSlice& sl = slices[threadIdx.x >> 5];
@@ -161,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(EngineArgs a, Segs segs) {
       const int64_t ra = r;
 
       if (a.bucket_bounds) {
-        int b = bucket_of(a.bucket_bounds, a.nbuckets, x);
+        int b = bucket_of(a.bucket_bounds, a.nbuckets, a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x);
         if (b != cur_bucket) {
           fold();
           if (lane == 0 && cur_bucket >= 0 && acc) atomicAdd(&a.out[cur_bucket], acc);
@@ -172,22 +269,18 @@ __global__ void __launch_bounds__(kThreads) k_engine(EngineArgs a, Segs segs) {
         cur_bucket = 0;
       }
 
-      const int64_t t0 = __ldg(&a.tab_indptr[x]);
-      const int64_t d = __ldg(&a.tab_indptr[x + 1]) - t0;
+      const int64_t u = a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x;
+      const int64_t t0 = __ldg(&a.tab_indptr[u]);
+      const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
       if (d > 0) {
         const bool small = d <= kTabCap;
         int32_t tmin, tmax;
-        int shift = 0;
         const int32_t* gtab = a.tab_indices + t0;
         if (small) {
-          int lb = 32 - __clz((int)(d - 1));  // ceil(log2 d)
-          int logbits = min(max(lb + 6, 10), 13);
-          shift = 32 - logbits;
           for (int i = lane; i < d; i += 32) {
             int32_t w = __ldg(&gtab[i]);
             sl.tab[i] = w;
-            uint32_t h = hash32((uint32_t)w) >> shift;
-            atomicOr(&sl.bm[h >> 5], 1u << (h & 31));
+            filt_insert(sl.bm, w);
           }
           __syncwarp();
           tmin = sl.tab[0];
@@ -208,42 +301,27 @@ __global__ void __launch_bounds__(kThreads) k_engine(EngineArgs a, Segs segs) {
           int64_t cs = __shfl_sync(FULL, s, src);
           int clen = __shfl_sync(FULL, len, src);
           if (lane >= nseg) clen = 0;
-          // exclusive prefix of lengths
-          int incl = clen;
+          // chunk span of each segment: [cs >> 2, (cs + clen + 3) >> 2)
+          const int64_t c0s = cs >> 2;
+          const int nch = (lane < nseg) ? (int)(((cs + clen + 3) >> 2) - c0s) : 0;
+          const int edge = (int)(cs & 3) | ((int)(((cs + clen - 1) & 3) + 1) << 2);
+          int incl = nch;  // inclusive prefix of chunk counts
           for (int o = 1; o < 32; o <<= 1) {
             int y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
           }
           const int total = __shfl_sync(FULL, incl, 31);
-          const int excl = incl - clen;
-          for (int base = 0; base < total; base += 32) {
-            unsigned cov = __ballot_sync(FULL, lane < nseg && excl <= base);
-            int c0 = __popc(cov) - 1;
-            unsigned bit = (lane < nseg && excl > base && excl < base + 32) ? (1u << (excl - base)) : 0u;
-            unsigned starts = __reduce_or_sync(FULL, bit);
-            int sj = c0 + __popc(starts & ((2u << lane) - 1u));
-            int64_t ss = __shfl_sync(FULL, cs, sj);
-            int se = __shfl_sync(FULL, excl, sj);
-            int f = base + lane;
-            if (f < total) {
-              int32_t w = __ldg(&a.pool[ss + (f - se)]);
-              if (w >= tmin && w <= tmax) {
-                if (small) {
-                  uint32_t h = hash32((uint32_t)w) >> shift;
-                  if ((sl.bm[h >> 5] >> (h & 31)) & 1u) cnt += bsearch_smem(sl.tab, (int)d, w);
-                } else {
-                  cnt += bsearch_gmem(gtab, d, w);
-                }
-              }
-            }
-          }
+          const int excl = incl - nch;
+          const int64_t delta = c0s - excl;  // flat chunk f of this segment: pool4[delta + f]
+          const int4* pool4 = reinterpret_cast<const int4*>(a.pool);
+          if (small)
+            probe_group<true>(pool4, sl, gtab, d, tmin, tmax, nseg, excl, incl, edge, delta, total, lane, cnt);
+          else
+            probe_group<false>(pool4, sl, gtab, d, tmin, tmax, nseg, excl, incl, edge, delta, total, lane, cnt);
         }
-        if (small) {  // clear the bits this owner set
+        if (small) {  // clear the words this owner set
           __syncwarp();
-          for (int i = lane; i < d; i += 32) {
-            uint32_t h = hash32((uint32_t)sl.tab[i]) >> shift;
-            sl.bm[h >> 5] = 0;
-          }
+          for (int i = lane; i < d; i += 32) sl.bm[filt_hash((uint32_t)sl.tab[i]) >> 23] = 0;
           __syncwarp();
         }
       }
@@ -258,13 +336,18 @@ __global__ void __launch_bounds__(kThreads) k_engine(EngineArgs a, Segs segs) {
 
 // Chunk schedule in cost space (see file header).  Thread i computes the
 // i-th boundary; thread 0 also publishes the chunk count.
+// mode 0 (paper): first half of the cost in one chunk per warp (Eq. 1),
+// then geometric chunks.  mode 1 (L2-tiled owners): the first 3/4 in
+// uniform chunks of 1/8 per-warp share, consumed in owner order so the
+// active window stays inside one or two tiles, then the geometric tail.
 __global__ void k_plan(const int64_t* __restrict__ cp, const int64_t* __restrict__ row_indptr,
                        int64_t x0, int64_t x1, int nW, int nmax, int64_t* chunk_r,
-                       int32_t* chunk_x, int* nchunks) {
+                       int32_t* chunk_x, int* nchunks, int mode) {
   const int64_t base = cp[x0];
   const int64_t C = cp[x1] - base;
   const double Cd = (double)C;
-  const double half = floor(Cd / 2.0);
+  const int nfirst = mode == 0 ? nW : 6 * nW;
+  const double half = mode == 0 ? floor(Cd / 2.0) : floor(Cd * 0.75);
   const double R0 = Cd - half;
   const double q = 1.0 - 1.0 / (double)nW;
   const double minc = fmax(Cd / (32.0 * nW), 64.0);
@@ -273,16 +356,16 @@ __global__ void k_plan(const int64_t* __restrict__ cp, const int64_t* __restrict
   if (J < 0) J = 0;
   const double RJ = R0 * pow(q, (double)J);
   const int64_t ntail = (int64_t)ceil(RJ / minc);
-  int64_t total = (C == 0) ? 0 : (int64_t)nW + J + ntail;
+  int64_t total = (C == 0) ? 0 : (int64_t)nfirst + J + ntail;
   if (total > nmax) total = nmax;
   if (blockIdx.x == 0 && threadIdx.x == 0) *nchunks = (int)total;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nmax;
        i += (int64_t)gridDim.x * blockDim.x) {
     double t;
     if (i >= total) t = Cd;
-    else if (i <= nW) t = floor((double)i * half / (double)nW);
+    else if (i <= nfirst) t = floor((double)i * half / (double)nfirst);
     else {
-      int64_t j = i - nW;
+      int64_t j = i - nfirst;
       if (j <= J) t = half + R0 * (1.0 - pow(q, (double)j));
       else t = half + (R0 - RJ) + (double)(j - J) * minc;
     }
@@ -356,18 +439,18 @@ template <class Segs>
 void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* row_indptr, const int64_t* tab_indptr,
                 const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
                 const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
-                cudaStream_t s) {
+                cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
   int blocks = engine_blocks();
   int nW = blocks * kWarps;
-  int nmax = 5 * nW + 8;
+  int nmax = 10 * nW + 8;
   int64_t* chunk_r = sc.alloc<int64_t>(nmax + 1);
   int32_t* chunk_x = sc.alloc<int32_t>(nmax);
   int* ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
   TC_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
-  k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(cp, row_indptr, x0, x1, nW, nmax, chunk_r, chunk_x, ctl);
+  k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(cp, row_indptr, x0, x1, nW, nmax, chunk_r, chunk_x, ctl, mode);
   check_launch();
   EngineArgs a{row_indptr, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
-               bucket_bounds, nbuckets, out, n_owner};
+               bucket_bounds, nbuckets, out, n_owner, owner_map};
   if (g_time_engine) {
     if (!g_ev[0]) {
       TC_CUDA(cudaEventCreate(&g_ev[0]));
@@ -394,11 +477,26 @@ void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const i
   TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
   TC_REQUIRE(nbuckets >= 1, TC_EINVAL, "nbuckets must be >= 1");
   TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
+  TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned (and padded to a multiple of 4 ids)");
   TC_CUDA(cudaMemsetAsync(out, 0, nbuckets * sizeof(unsigned long long), s));
   if (u1 <= u0) return;
   Scratch sc(s);
   run_engine(sc, n, rev_cost, rev_indptr, tab_indptr, tab_indices, pool, u0, u1, bucket_bounds,
-             nbuckets, out, PullSegs{reinterpret_cast<const longlong2*>(rev_seg)}, s);
+             nbuckets, out, PullSegs{reinterpret_cast<const longlong2*>(rev_seg)}, s, nullptr, 1);
+}
+
+void count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
+                  const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                  const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int nbuckets,
+                  unsigned long long* out, int mode, cudaStream_t s) {
+  TC_REQUIRE(k >= 0 && nbuckets >= 1, TC_EINVAL, "bad owner count / nbuckets");
+  TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
+  TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned (and padded to a multiple of 4 ids)");
+  TC_CUDA(cudaMemsetAsync(out, 0, nbuckets * sizeof(unsigned long long), s));
+  if (k == 0) return;
+  Scratch sc(s);
+  run_engine(sc, k, cost_prefix, row_indptr, tab_indptr, tab_indices, pool, 0, k, bucket_bounds,
+             nbuckets, out, PullSegs{reinterpret_cast<const longlong2*>(segs)}, s, owner_map, mode);
 }
 
 void count_lowest(const int64_t* indptr, const int32_t* indices, int64_t n, int64_t v0, int64_t v1,
@@ -407,6 +505,7 @@ void count_lowest(const int64_t* indptr, const int32_t* indices, int64_t n, int6
   TC_REQUIRE(0 <= v0 && v0 <= v1 && v1 <= n, TC_EINVAL, "bad node range");
   TC_REQUIRE(nbuckets >= 1, TC_EINVAL, "nbuckets must be >= 1");
   TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
+  TC_REQUIRE(((uintptr_t)indices & 15) == 0, TC_EINVAL, "indices must be 16-byte aligned (and padded to a multiple of 4 ids)");
   TC_CUDA(cudaMemsetAsync(out, 0, nbuckets * sizeof(unsigned long long), s));
   if (v1 <= v0) return;
   Scratch sc(s);
@@ -478,6 +577,16 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
   return tcb::guarded([&] {
     tcb::count_middle(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, n, u0, u1,
                       bucket_bounds, nbuckets, out, (cudaStream_t)stream);
+  });
+}
+
+int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
+                    const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                    const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int32_t nbuckets,
+                    unsigned long long* out, int32_t mode, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    tcb::count_owners(tab_indptr, tab_indices, owner_map, row_indptr, segs, cost_prefix, pool, k,
+                      bucket_bounds, nbuckets, out, mode, (cudaStream_t)stream);
   });
 }
 

@@ -16,6 +16,7 @@ everywhere).  Besides the reference's fields the Graph keeps the reverse
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -137,6 +138,47 @@ class Graph:
                     eff_deg=f(self.eff_deg))
 
 
+# List entries per L2 tile of the optional tiled predecessor index (0 = off).
+TILE_IDS = int(os.environ.get("TCB_TILE_IDS", "0"))
+
+
+@dataclass
+class TiledIndex:
+    """Predecessor entries of u in [u0, u1) regrouped tile-major (csrc/tile.cu)."""
+
+    u0: int
+    u1: int
+    k: int
+    ntiles: int
+    owner_u: torch.Tensor
+    owner_ptr: torch.Tensor
+    segs: torch.Tensor
+    cost: torch.Tensor
+
+
+def tiled_index(g: "Graph", u0: int, u1: int) -> TiledIndex:
+    key = ("tiled", u0, u1, TILE_IDS)
+    t = g._cache.get(key)
+    if t is None:
+        dev = g.eff_indptr.device
+        E = int(g._rev_indptr[u1] - g._rev_indptr[u0]) if g.n else 0
+        owner_u = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+        owner_ptr = torch.empty(E + 1, dtype=torch.int64, device=dev)
+        segs = torch.empty(max(2 * E, 2), dtype=torch.int64, device=dev)
+        cost = torch.empty(E + 1, dtype=torch.int64, device=dev)
+        k, nt = ctypes.c_int64(), ctypes.c_int64()
+        if g.n:
+            _lib.call("tc_tile_pull", _lib.ptr(g.eff_indptr), g.n, _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_src),
+                      _lib.ptr(g._rev_seg), u0, u1, TILE_IDS, _lib.ptr(owner_u), _lib.ptr(owner_ptr),
+                      _lib.ptr(segs), _lib.ptr(cost), ctypes.byref(k), ctypes.byref(nt), _lib.stream())
+        else:
+            owner_ptr.zero_()
+            cost.zero_()
+        t = TiledIndex(u0, u1, k.value, nt.value, owner_u, owner_ptr, segs, cost)
+        g._cache[key] = t
+    return t
+
+
 def normalize(raw: RawGraph) -> RawGraph:
     """Drop self-loops, collapse duplicate undirected edges and compact labels
     to 0..n-1 (graph.py:76-103), on the device.  Dense labels are kept as-is;
@@ -160,7 +202,8 @@ def _assemble(raw: RawGraph, order) -> Graph:
     n, m = int(raw.n), int(e.shape[0])
     i64 = lambda k: torch.empty(max(k, 1), dtype=torch.int64, device=dev)  # noqa: E731
     i32 = lambda k: torch.empty(max(k, 1), dtype=torch.int32, device=dev)  # noqa: E731
-    eff_indptr, eff_indices = i64(n + 1), i32(m)
+    # +4 ids of padding: the engines read lists as 16-byte chunks
+    eff_indptr, eff_indices = i64(n + 1), i32(m + 4)
     relabel, orig_ids, deg, eff_deg = i32(n), i32(n), i32(n), i32(n)
     rev_indptr, rev_src, rev_seg, rev_cost = i64(n + 1), i32(m), i64(2 * m), i64(n + 1)
     order_t = None
@@ -170,8 +213,11 @@ def _assemble(raw: RawGraph, order) -> Graph:
               _lib.ptr(eff_indices), _lib.ptr(relabel), _lib.ptr(orig_ids), _lib.ptr(deg),
               _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_src), _lib.ptr(rev_seg),
               _lib.ptr(rev_cost), _lib.stream())
-    return Graph(n, m, eff_indptr[: n + 1], eff_indices[:m], relabel[:n], orig_ids[:n], deg[:n],
-                 eff_deg[:n], rev_indptr[: n + 1], rev_src[:m], rev_seg[: 2 * m], rev_cost[: n + 1])
+    g = Graph(n, m, eff_indptr[: n + 1], eff_indices[:m], relabel[:n], orig_ids[:n], deg[:n],
+              eff_deg[:n], rev_indptr[: n + 1], rev_src[:m], rev_seg[: 2 * m], rev_cost[: n + 1])
+    if TILE_IDS:
+        tiled_index(g, 0, n)  # optional L2-tiled predecessor index, built with the graph
+    return g
 
 
 def build_graph(raw: RawGraph) -> Graph:

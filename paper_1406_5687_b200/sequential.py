@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .graph import Graph
+from .graph import Graph, tiled_index
 
 BRUTE_MAX_NODES = 2000
 
@@ -38,13 +38,26 @@ def intersect_count(a, b) -> int:
     return int(out.item())
 
 
-def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None):
+def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
     """Middle-vertex engine over u in [u0, u1), optionally binned by `bounds`
-    (device int64[k+1]).  Returns the device uint64 counts (as int64)."""
+    (device int64[k+1]).  Returns the device uint64 counts (as int64).
+
+    tiled=True runs over the L2-tiled predecessor index of the range
+    (graph.tiled_index, cached on the graph); the default follows
+    TCB_TILE_IDS (off unless set)."""
     u1 = g.n if u1 is None else u1
+    if tiled is None:
+        from .graph import TILE_IDS
+        tiled = TILE_IDS > 0
     k = 1 if bounds is None else int(bounds.numel()) - 1
     if out is None:
         out = torch.empty(k, dtype=torch.int64, device=g.eff_indptr.device)
+    if tiled:
+        t = tiled_index(g, int(u0), int(u1))
+        _lib.call("tc_count_owners", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(t.owner_u),
+                  _lib.ptr(t.owner_ptr), _lib.ptr(t.segs), _lib.ptr(t.cost), _lib.ptr(g.eff_indices), t.k,
+                  _lib.ptr(bounds), k, _lib.ptr(out), 1, _lib.stream())
+        return out
     _lib.call("tc_count_middle", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices),
               _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost),
               _lib.ptr(g.eff_indices), g.n, int(u0), int(u1), _lib.ptr(bounds), k, _lib.ptr(out),

@@ -50,10 +50,12 @@ def surrogate_count(x, core: NodeRange, g: Graph) -> int:
     lists of x's members inside `core` (space_efficient.py:66-74;
     _kernels.py:70-80), on the device via the middle-vertex engine."""
     dev = g.eff_indptr.device
-    xs = torch.as_tensor(np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x, dtype=np.int64)
-                         .astype(np.int32)).to(dev)
-    if xs.numel() == 0 or core.count == 0:
+    xh = np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x, dtype=np.int64).astype(np.int32)
+    if xh.size == 0 or core.count == 0:
         return 0
+    buf = torch.zeros(xh.size + 4, dtype=torch.int32, device=dev)  # padded for 16-byte chunk reads
+    buf[: xh.size] = torch.as_tensor(xh).to(dev)
+    xs = buf[: xh.size]
     offs = torch.tensor([0, xs.numel()], dtype=torch.int64, device=dev)
     segs_owner, segs, nseg = owner_segments(offs, xs, core.start, core.stop, 0)
     return count_segments(g.eff_indptr[core.start:], g.eff_indices, xs, segs_owner, segs, nseg,
