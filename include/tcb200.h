@@ -136,6 +136,11 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
  * launch on (1) or off (0).  Bracketing synchronises after each launch. */
 int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host);
 
+/* Engine tier caps (testing / tuning): key 0 = warp-tier table cap
+ * (0..256, default 256), key 1 = block-tier staged-table cap (0..4096,
+ * default 4096; larger tables use binary search in global memory). */
+int tc_set_tuning(int32_t key, int64_t value);
+
 /* |a ∩ b| of two strictly ascending int32 lists (_kernels.py:15-37). */
 int tc_intersect_count(const int32_t* a, int64_t na, const int32_t* b, int64_t nb,
                        unsigned long long* out, tc_stream_t stream);

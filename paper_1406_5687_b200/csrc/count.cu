@@ -3,31 +3,36 @@
 // Work model.  Every triangle v < u < w (canonical degree order) is found by
 // probing list elements into a shared-memory table:
 //
-//   pull ("middle vertex", tc_count_middle): owner = u.  Table = N^_u;
-//        segments = for each predecessor v of u, the suffix of N^_v after u
-//        (rev_seg).  Probes per graph = sum_v C(d^_v, 2), 2-5x fewer than the
-//        merge model's W -- the headline path.
+//   pull ("middle vertex", tc_count_middle / tc_count_owners): owner = u.
+//        Table = N^_u; segments = for each predecessor v of u, the suffix of
+//        N^_v after u (rev_seg).  Probes = sum_v C(d^_v, 2), 2-5x fewer than
+//        the merge model's W -- the headline path.
 //   push ("lowest vertex", tc_count_lowest): owner = v.  Table = N^_v;
 //        segments = N^_u for every u in N^_v.  This is exactly
 //        count_node_range(v0, v1) (_kernels.py:40-52) with per-bucket
 //        partials, used for count_task / count_dynamic.
 //
-// A warp owns one owner at a time: it stages the owner's list in its
-// shared-memory slice (sorted copy + hashed bitmap filter), then streams the
-// owner's segments 32 probes per step: segments are compacted across lanes,
-// flattened with a warp scan, and each lane resolves its segment with one
-// ballot + one redux.or + popc (no per-probe search).  A probe is a range
-// check, one bitmap LDS, and -- only for bitmap hits -- a binary search in
-// the sorted copy.  Lists longer than the shared slice fall back to binary
-// search in global memory (L1/L2 resident).
+// Two tiers by table size (the shape-bucketing of SURVEY.md §7 step 6):
+//   warp tier  (d <= 256): a warp stages the owner's list in its own
+//              shared-memory slice -- sorted copy + 16K-bit hashed filter.
+//   block tier (d  > 256): a 512-thread block stages up to 16K entries plus
+//              a 1M-bit filter (192 KB) and all 16 warps stream the owner's
+//              segments -- the skewed pairs of Chung-Lu / R-MAT hubs.
+//              Beyond 16K entries the probes fall back to binary search in
+//              global memory (L1/L2 resident).
+// Segment streaming (both tiers): a warp takes 32 segments, compacts the
+// non-empty ones, and flattens the 16-byte chunks they touch with a warp
+// scan; lane j of a window loads chunk base+j as one int4 (4 list ids),
+// resolving its segment with one ballot + one redux.or + popc.  A probe is a
+// range check, one filter LDS and three ALU ops, branch-free over the 4 ids;
+// only filter hits take the binary-search verification in the sorted copy.
 //
 // Load balance (the paper's dynamic load balancing, PAPER.md:788-822,
-// dynamic_lb.py:68-109, restated for warps): the owner-cost prefix is split
-// in cost space -- the first half into one equal chunk per warp, then
-// geometrically shrinking chunks of (remaining / warps), then fixed minimum
-// chunks -- and chunk boundaries fall INSIDE an owner's segment list, so a
-// hub never pins a warp.  Warps pull chunk indices from one global atomic
-// counter (the coordinator's queue).
+// dynamic_lb.py:68-109, restated for warps): each tier splits its owners'
+// cost prefix into chunks whose boundaries fall INSIDE an owner's segment
+// list (so a hub never pins a warp), ending with the paper's geometrically
+// shrinking tasks of (remaining / workers); workers pull chunk indices from
+// one global atomic counter (the coordinator's queue).
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -40,17 +45,30 @@ namespace tcb {
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
-static constexpr int kWarps = 8;          // warps per block
+static constexpr int kWarps = 8;          // warps per block (warp tier)
 static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
-static constexpr int kTabCap = 256;       // sorted-table capacity per warp (elements)
-static constexpr int kBmWords = 512;      // filter words per warp (16384 bits)
+static constexpr int kTabCap = 256;       // warp tier: ids per table (sorted copy)
+static constexpr int kLwWarp = 9;         // warp tier filter: 2^9 words = 16K bits (2 KB)
+static constexpr int kBigThreads = 512;   // block tier
+static constexpr int kBigWarps = kBigThreads / 32;
+static constexpr int kBigCap = 4096;      // block tier: ids per staged table
+static constexpr int kLwBig = 13;         // block tier filter: 2^13 words = 256K bits (32 KB)
+static constexpr int kLbBig = 11;         // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
+static constexpr int kPosCap = 512;       // block tier: per-warp queue of filter hits
+static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
+static constexpr size_t kBigSmem = (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
+                                   sizeof(int32_t) * kPosCap * kBigWarps;
 static constexpr int kSegCost = 2;        // must match build.cu
 static constexpr int kTabCost = 16;
+static constexpr int32_t kEmpty = -1;
+
+// Verification kinds of a staged table (see probe4).
+enum : int { kGlobal = 0, kSorted = 1, kBuckets = 2 };
 
 struct WarpSlice {
   int32_t tab[kTabCap];
-  uint32_t bm[kBmWords];
+  uint32_t bm[1 << kLwWarp];
 };
 
 // --------------------------------------------------------------- segments
@@ -74,7 +92,62 @@ struct PushSegs {  // forward edge e of v -> N^_u, u = indices[e]
   }
 };
 
-__device__ __forceinline__ uint32_t hash32(uint32_t w) { return w * 0x9E3779B1u; }
+// Per-owner tables.  Every staged table has a hashed one-bit filter in
+// front (2^lw words, h = id * golden, word = h >> (32 - lw), bit =
+// (h >> (27 - lw)) & 31): a probe is one LDS.32 and three ALU ops, and only
+// filter hits (true hits plus ~d/2^(lw+5) false positives) are verified:
+//   kSorted  (warp tier): binary search in a sorted shared copy, inline --
+//            cheapest when hits are rare (PA: 0.4% of probes);
+//   kBuckets (block tier): hits are queued per warp and verified in bulk
+//            against a bucketized hash table (2^lb buckets of 4 ids,
+//            bucket = h >> (32 - lb), overflow to the next bucket, load
+//            <= 1/2): one LDS.128 per hit -- for hubs, where hit rates
+//            reach ~40% (R-MAT) and a 12-step binary search per hit would
+//            dominate;
+//   kGlobal  (beyond the block cap): binary search in global memory.
+__device__ __forceinline__ uint32_t tab_hash(uint32_t w) { return w * 0x9E3779B1u; }
+
+__device__ __forceinline__ int tab_lb(int64_t d) {  // log2 buckets: smallest 2^lb >= d/2, >= 8
+  int64_t want = (d + 1) / 2;
+  int lb = 32 - __clz((int)(want > 2 ? want - 1 : 1));
+  return max(lb, 3);
+}
+
+template <int kLw>
+__device__ __forceinline__ void filt_insert(uint32_t* bm, int32_t w) {
+  const uint32_t h = tab_hash((uint32_t)w);
+  atomicOr(&bm[h >> (32 - kLw)], 1u << ((h >> (27 - kLw)) & 31));
+}
+
+template <int kLw>
+__device__ __forceinline__ void filt_clear(uint32_t* bm, int32_t w) {
+  bm[tab_hash((uint32_t)w) >> (32 - kLw)] = 0;
+}
+
+__device__ __forceinline__ void bkt_insert(int4* bkt, int lb, int32_t w) {
+  int32_t* slots = reinterpret_cast<int32_t*>(bkt);
+  const uint32_t mask = (1u << lb) - 1;
+  uint32_t b = tab_hash((uint32_t)w) >> (32 - lb);
+  for (;;) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (atomicCAS(&slots[b * 4 + k], kEmpty, w) == kEmpty) return;
+    b = (b + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ bool bkt_has(int4 q, int32_t x) { return (q.x == x) | (q.y == x) | (q.z == x) | (q.w == x); }
+
+__device__ __forceinline__ bool bkt_lookup(const int4* bkt, int lb, int32_t x) {
+  const uint32_t mask = (1u << lb) - 1;
+  uint32_t b = tab_hash((uint32_t)x) >> (32 - lb);
+  for (;;) {
+    int4 q = bkt[b];
+    if (bkt_has(q, x)) return true;
+    if (q.w == kEmpty) return false;
+    b = (b + 1) & mask;
+  }
+}
 
 __device__ __forceinline__ bool bsearch_smem(const int32_t* t, int d, int32_t w) {
   int lo = 0, hi = d;
@@ -96,73 +169,76 @@ __device__ __forceinline__ bool bsearch_gmem(const int32_t* __restrict__ t, int6
   return lo < d && __ldg(&t[lo]) == w;
 }
 
-struct EngineArgs {
-  const int64_t* row_indptr;  // owner -> segment index range
-  const int64_t* tab_indptr;  // owner -> table list
-  const int32_t* tab_indices;
-  const int32_t* pool;        // segment coordinates index this array
-  const int64_t* chunk_r;     // [nmax+1] segment-index chunk boundaries
-  const int32_t* chunk_x;     // [nmax] owner at chunk start
-  const int* nchunks;
-  int* queue;
-  const int64_t* bucket_bounds;  // nullable; bins owners
-  int nbuckets;
-  unsigned long long* out;
-  int64_t n_owner;            // row_indptr has n_owner + 1 entries
-  const int32_t* owner_map;   // nullable: owner x -> table/bucket node id
+struct Table {
+  const uint32_t* bm;   // filter (kSorted, kBuckets)
+  const int32_t* tab;   // sorted shared copy (kSorted) or global list (kGlobal)
+  const int4* bkt;      // buckets (kBuckets)
+  int32_t* pos;         // per-warp hit queue (kBuckets)
+  int64_t d;
+  int lb;
+  int32_t tmin, tmax;
 };
 
-__device__ __forceinline__ int bucket_of(const int64_t* bb, int nb, int64_t x) {
-  if (!bb) return 0;
-  int lo = 0, hi = nb;  // largest b with bb[b] <= x
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (__ldg(&bb[mid]) <= x) lo = mid;
-    else hi = mid;
-  }
-  return lo;
+// Verify the queued filter hits of this warp (kBuckets) and empty the queue.
+__device__ __forceinline__ void drain(const Table& t, int& npos, int lane, uint32_t& cnt) {
+  __syncwarp();
+  for (int i = lane; i < npos; i += 32) cnt += bkt_lookup(t.bkt, t.lb, t.pos[i]);
+  __syncwarp();
+  npos = 0;
 }
 
-// Hashed one-bit filter over one owner's list: bit (h >> 18) of the 16K-bit
-// word array (word h >> 23, bit (h >> 18) & 31), h = w * golden.  A probe is
-// one LDS and three ALU ops; the false-positive rate is d / 16384 per probe,
-// and positives are verified by binary search in the sorted copy.
-__device__ __forceinline__ uint32_t filt_hash(uint32_t w) { return w * 0x9E3779B1u; }
-
-__device__ __forceinline__ void filt_insert(uint32_t* bm, int32_t w) {
-  uint32_t h = filt_hash((uint32_t)w);
-  atomicOr(&bm[h >> 23], 1u << ((h >> 18) & 31));
-}
-
-// 4-bit mask of the elements of v (valid ones per vmask) that pass the
-// range check and hit the filter.  Branch-free.
-__device__ __forceinline__ uint32_t filt_probe4(const uint32_t* bm, int4 v, uint32_t vmask, int32_t tmin,
-                                                int32_t tmax) {
-  uint32_t m = 0;
+template <int kKind, int kLw>
+__device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, int lane, int& npos, uint32_t& cnt) {
   int32_t xs[4] = {v.x, v.y, v.z, v.w};
+  if (kKind == kGlobal) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((vmask >> k) & 1u) && xs[k] >= t.tmin && xs[k] <= t.tmax) cnt += bsearch_gmem(t.tab, t.d, xs[k]);
+    return;
+  }
+  uint32_t m = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    uint32_t h = filt_hash((uint32_t)xs[k]);
-    uint32_t wd = bm[h >> 23];
-    uint32_t bit = (wd >> ((h >> 18) & 31)) & 1u;
-    bool in = ((vmask >> k) & 1u) && xs[k] >= tmin && xs[k] <= tmax;
+    const uint32_t h = tab_hash((uint32_t)xs[k]);
+    const uint32_t bit = (t.bm[h >> (32 - kLw)] >> ((h >> (27 - kLw)) & 31)) & 1u;
+    const bool in = ((vmask >> k) & 1u) && xs[k] >= t.tmin && xs[k] <= t.tmax;
     m |= (in ? bit : 0u) << k;
   }
-  return m;
+  if (kKind == kSorted) {
+    if (m) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((m >> k) & 1u) cnt += bsearch_smem(t.tab, (int)t.d, xs[k]);
+    }
+    return;
+  }
+  const unsigned FULL = 0xffffffffu;  // kBuckets: warp-aggregated append
+  if (__any_sync(FULL, m != 0)) {
+    const int c = __popc(m);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int at = npos + incl - c;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((m >> k) & 1u) t.pos[at++] = xs[k];
+    npos += __shfl_sync(FULL, incl, 31);
+  }
 }
 
-// Resolve the probes of one group of <= 32 compacted segments.  The group is
-// flattened over the 16-byte chunks its segments touch: lane j of window k
-// loads chunk base+32k+j as one int4 (4 list elements) and probes the
-// elements of it that lie inside its segment.  Two windows are in flight.
+// Probes of one group of <= 32 compacted segments.  The group is flattened
+// over the 16-byte chunks its segments touch: lane j of window k loads
+// chunk base+32k+j as one int4 and probes the ids of it inside its segment.
 // Segment s covers chunks [excl_s, endx_s) of the flat space; chunk f of it
 // is pool4[delta_s + f]; `edge_s` packs (first-chunk offset | last-chunk
 // count << 2).
-template <bool kSmall>
-__device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const WarpSlice& sl,
-                                            const int32_t* __restrict__ gtab, int64_t d, int32_t tmin,
-                                            int32_t tmax, int nseg, int excl, int endx, int edge,
-                                            int64_t delta, int total, int lane, uint32_t& cnt) {
+template <int kKind, int kLw>
+__device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
+                                            int endx, int edge, int64_t delta, int total, int lane,
+                                            int& npos, uint32_t& cnt) {
   const unsigned FULL = 0xffffffffu;
   const bool lane_seg = lane < nseg;
   for (int base = 0; base < total; base += 32 * kWin) {
@@ -193,25 +269,110 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
       }
     }
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) {
-      if (kSmall) {
-        uint32_t m = filt_probe4(sl.bm, v[k], vm[k], tmin, tmax);
-        if (m) {
-          int32_t xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if ((m >> e) & 1u) cnt += bsearch_smem(sl.tab, (int)d, xs[e]);
-        }
-      } else {
-        int32_t xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (((vm[k] >> e) & 1u) && xs[e] >= tmin && xs[e] <= tmax) cnt += bsearch_gmem(gtab, d, xs[e]);
-      }
-    }
+    for (int k = 0; k < kWin; ++k) probe4<kKind, kLw>(t, v[k], vm[k], lane, npos, cnt);
+    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
   }
 }
 
+// One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner.
+template <int kKind, int kLw, class Segs>
+__device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
+                                             int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt) {
+  const unsigned FULL = 0xffffffffu;
+  int64_t s = 0, e = 0;
+  if (g0 + lane < g1) segs.get(g0 + lane, s, e);
+  int len = (int)(e - s);
+  unsigned nz = __ballot_sync(FULL, len > 0);  // compact non-empty segments to the low lanes
+  int nseg = __popc(nz);
+  int src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
+  int64_t cs = __shfl_sync(FULL, s, src);
+  int clen = __shfl_sync(FULL, len, src);
+  if (lane >= nseg) clen = 0;
+  // chunk span of each segment: [cs >> 2, (cs + clen + 3) >> 2)
+  const int64_t c0s = cs >> 2;
+  const int nch = (lane < nseg) ? (int)(((cs + clen + 3) >> 2) - c0s) : 0;
+  const int edge = (int)(cs & 3) | ((int)(((cs + clen - 1) & 3) + 1) << 2);
+  int incl = nch;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(FULL, incl, 31);
+  const int excl = incl - nch;
+  probe_group<kKind, kLw>(reinterpret_cast<const int4*>(pool), t, nseg, excl, incl, edge, c0s - excl, total, lane,
+                          npos, cnt);
+}
+
+struct EngineArgs {
+  const int64_t* row_indptr;  // owner -> segment index range
+  const int64_t* tab_indptr;  // node -> table list
+  const int32_t* tab_indices;
+  const int32_t* pool;        // segment coordinates index this array
+  const int64_t* chunk_r;     // [nmax+1] segment-index chunk boundaries
+  const int32_t* chunk_x;     // [nmax] owner at chunk start
+  const int* nchunks;
+  int* queue;
+  const int64_t* bucket_bounds;  // nullable; bins owner_map(x)
+  int nbuckets;
+  unsigned long long* out;
+  int64_t n_owner;            // row_indptr has n_owner + 1 entries
+  const int32_t* owner_map;   // nullable: owner x -> table/bucket node id
+  int warp_cap;               // tables with d <= warp_cap use the warp tier
+  int big_cap;                // block tier stages d <= big_cap, else global search
+};
+
+// Runtime tier caps (tc_set_tuning; tests lower them to force every tier).
+static int g_warp_cap = kTabCap;
+static int g_big_cap = kBigCap;
+
+__device__ __forceinline__ int bucket_of(const int64_t* bb, int nb, int64_t x) {
+  if (!bb) return 0;
+  int lo = 0, hi = nb;  // largest b with bb[b] <= x
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(&bb[mid]) <= x) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// First owner >= x whose segment row ends after r (warp-cooperative skip).
+__device__ __forceinline__ int64_t advance_owner(const EngineArgs& a, int64_t x, int64_t r, int lane) {
+  for (;;) {
+    int64_t idx = x + 1 + lane;
+    int64_t nx = (idx <= a.n_owner) ? __ldg(&a.row_indptr[idx]) : INT64_MAX;
+    unsigned past = __ballot_sync(0xffffffffu, nx > r);
+    if (past) return x + __ffs(past) - 1;
+    x += 32;
+  }
+}
+
+// Per-warp accumulation, flushed per bucket.
+struct Acc {
+  unsigned long long acc = 0;  // same on all lanes
+  int cur = -1;
+  uint32_t cnt = 0;            // per-lane hits since the last fold
+  __device__ __forceinline__ void fold() {
+    unsigned long long t = cnt;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    acc += t;
+    cnt = 0;
+  }
+  __device__ __forceinline__ void flush(unsigned long long* out, int lane) {
+    if (lane == 0 && cur >= 0 && acc) atomicAdd(&out[cur], acc);
+    acc = 0;
+  }
+  __device__ __forceinline__ void to_bucket(const EngineArgs& a, int64_t u, int lane) {
+    int b = a.bucket_bounds ? bucket_of(a.bucket_bounds, a.nbuckets, u) : 0;
+    if (b != cur) {
+      fold();
+      flush(a.out, lane);
+      cur = b;
+    }
+  }
+};
+
+// Warp tier: owners with d <= kTabCap (larger ones belong to k_engine_big).
 template <class Segs>
 __global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSlice slices[kWarps];
@@ -219,18 +380,9 @@ __global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a
   WarpSlice& sl = slices[threadIdx.x >> 5];
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
-  for (int i = lane; i < kBmWords; i += 32) sl.bm[i] = 0;
+  for (int i = lane; i < (1 << kLwWarp); i += 32) sl.bm[i] = 0;
   __syncwarp();
-
-  unsigned long long acc = 0;  // warp total for the current bucket (same on all lanes)
-  int cur_bucket = -1;
-  uint32_t cnt = 0;            // per-lane hits since the last fold
-  auto fold = [&]() {
-    unsigned long long t = cnt;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-    acc += t;
-    cnt = 0;
-  };
+  Acc acc;
 
   for (;;) {
     int c = 0;
@@ -240,96 +392,108 @@ __global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a
     int64_t r = a.chunk_r[c];
     const int64_t r1 = a.chunk_r[c + 1];
     int64_t x = a.chunk_x[c];
-
     while (r < r1) {
-      // advance to the owner whose segment row contains r (skips empty rows)
-      for (;;) {
-        int64_t idx = x + 1 + lane;
-        int64_t nx = (idx <= a.n_owner) ? __ldg(&a.row_indptr[idx]) : INT64_MAX;
-        unsigned past = __ballot_sync(FULL, nx > r);
-        if (past) {
-          x += __ffs(past) - 1;
-          break;
-        }
-        x += 32;
-      }
+      x = advance_owner(a, x, r, lane);
       const int64_t xe_row = __ldg(&a.row_indptr[x + 1]);
       const int64_t rb = min(xe_row, r1);
       const int64_t ra = r;
-
-      if (a.bucket_bounds) {
-        int b = bucket_of(a.bucket_bounds, a.nbuckets, a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x);
-        if (b != cur_bucket) {
-          fold();
-          if (lane == 0 && cur_bucket >= 0 && acc) atomicAdd(&a.out[cur_bucket], acc);
-          acc = 0;
-          cur_bucket = b;
-        }
-      } else {
-        cur_bucket = 0;
-      }
-
+      r = rb;
       const int64_t u = a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x;
       const int64_t t0 = __ldg(&a.tab_indptr[u]);
       const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d > 0) {
-        const bool small = d <= kTabCap;
-        int32_t tmin, tmax;
-        const int32_t* gtab = a.tab_indices + t0;
-        if (small) {
-          for (int i = lane; i < d; i += 32) {
-            int32_t w = __ldg(&gtab[i]);
-            sl.tab[i] = w;
-            filt_insert(sl.bm, w);
-          }
-          __syncwarp();
-          tmin = sl.tab[0];
-          tmax = sl.tab[d - 1];
-        } else {
-          tmin = __ldg(&gtab[0]);
-          tmax = __ldg(&gtab[d - 1]);
-        }
-
-        for (int64_t g = ra; g < rb; g += 32) {
-          int64_t s = 0, e = 0;
-          if (g + lane < rb) segs.get(g + lane, s, e);
-          int len = (int)(e - s);
-          // compact non-empty segments to the low lanes
-          unsigned nz = __ballot_sync(FULL, len > 0);
-          int nseg = __popc(nz);
-          int src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
-          int64_t cs = __shfl_sync(FULL, s, src);
-          int clen = __shfl_sync(FULL, len, src);
-          if (lane >= nseg) clen = 0;
-          // chunk span of each segment: [cs >> 2, (cs + clen + 3) >> 2)
-          const int64_t c0s = cs >> 2;
-          const int nch = (lane < nseg) ? (int)(((cs + clen + 3) >> 2) - c0s) : 0;
-          const int edge = (int)(cs & 3) | ((int)(((cs + clen - 1) & 3) + 1) << 2);
-          int incl = nch;  // inclusive prefix of chunk counts
-          for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-          }
-          const int total = __shfl_sync(FULL, incl, 31);
-          const int excl = incl - nch;
-          const int64_t delta = c0s - excl;  // flat chunk f of this segment: pool4[delta + f]
-          const int4* pool4 = reinterpret_cast<const int4*>(a.pool);
-          if (small)
-            probe_group<true>(pool4, sl, gtab, d, tmin, tmax, nseg, excl, incl, edge, delta, total, lane, cnt);
-          else
-            probe_group<false>(pool4, sl, gtab, d, tmin, tmax, nseg, excl, incl, edge, delta, total, lane, cnt);
-        }
-        if (small) {  // clear the words this owner set
-          __syncwarp();
-          for (int i = lane; i < d; i += 32) sl.bm[filt_hash((uint32_t)sl.tab[i]) >> 23] = 0;
-          __syncwarp();
-        }
+      if (d <= 0 || d > a.warp_cap) continue;
+      acc.to_bucket(a, u, lane);
+      const int32_t* gtab = a.tab_indices + t0;
+      for (int i = lane; i < d; i += 32) {
+        const int32_t w = __ldg(&gtab[i]);
+        sl.tab[i] = w;
+        filt_insert<kLwWarp>(sl.bm, w);
       }
-      r = rb;
+      __syncwarp();
+      Table t{sl.bm, sl.tab, nullptr, nullptr, d, 0, sl.tab[0], sl.tab[d - 1]};
+      int npos = 0;
+      for (int64_t g = ra; g < rb; g += 32)
+        stream_group<kSorted, kLwWarp>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+      __syncwarp();
+      for (int i = lane; i < d; i += 32) filt_clear<kLwWarp>(sl.bm, sl.tab[i]);
+      __syncwarp();
     }
-    fold();
+    acc.fold();
   }
-  if (lane == 0 && cur_bucket >= 0 && acc) atomicAdd(&a.out[cur_bucket], acc);
+  acc.flush(a.out, lane);
+}
+
+// Block tier: owners with d > kTabCap.  The block stages the owner's table
+// once per chunk-owner and its 16 warps stream groups of 32 segments.
+template <class Segs>
+__global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Segs segs) {
+  extern __shared__ __align__(16) unsigned char big_smem[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(big_smem);
+  int4* bkt = reinterpret_cast<int4*>(big_smem + (sizeof(uint32_t) << kLwBig));
+  int32_t* pos = reinterpret_cast<int32_t*>(big_smem + (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig)) +
+                 (threadIdx.x >> 5) * kPosCap;
+  __shared__ int s_chunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kBigWarps;
+  const int nch = *a.nchunks;
+  for (int i = threadIdx.x; i < (1 << kLwBig); i += kBigThreads) bm[i] = 0;
+  Acc acc;
+  int64_t staged = -1;  // node whose table is staged
+  const int32_t* staged_list = nullptr;
+  int64_t staged_d = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(a.queue, 1);
+    __syncthreads();
+    const int c = s_chunk;
+    if (c >= nch) break;
+    int64_t r = a.chunk_r[c];
+    const int64_t r1 = a.chunk_r[c + 1];
+    int64_t x = a.chunk_x[c];
+    while (r < r1) {
+      x = advance_owner(a, x, r, lane);  // same result in every warp
+      const int64_t xe_row = __ldg(&a.row_indptr[x + 1]);
+      const int64_t rb = min(xe_row, r1);
+      const int64_t ra = r;
+      r = rb;
+      const int64_t u = a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x;
+      const int64_t t0 = __ldg(&a.tab_indptr[u]);
+      const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
+      if (d <= a.warp_cap) continue;
+      acc.to_bucket(a, u, lane);
+      const int32_t* gtab = a.tab_indices + t0;
+      const int lb = tab_lb(d);
+      if (d <= a.big_cap) {
+        if (staged != u) {
+          __syncthreads();
+          for (int i = threadIdx.x; i < staged_d; i += kBigThreads) filt_clear<kLwBig>(bm, __ldg(&staged_list[i]));
+          for (int i = threadIdx.x; i < (1 << lb); i += kBigThreads) bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
+          __syncthreads();
+          for (int i = threadIdx.x; i < d; i += kBigThreads) {
+            const int32_t w = __ldg(&gtab[i]);
+            filt_insert<kLwBig>(bm, w);
+            bkt_insert(bkt, lb, w);
+          }
+          __syncthreads();
+          staged = u;
+          staged_list = gtab;
+          staged_d = d;
+        }
+        Table t{bm, nullptr, bkt, pos, d, lb, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
+        int npos = 0;
+        for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
+          stream_group<kBuckets, kLwBig>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+        drain(t, npos, lane, acc.cnt);
+      } else {
+        Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
+        int npos = 0;
+        for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
+          stream_group<kGlobal, 0>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+      }
+    }
+    acc.fold();
+  }
+  acc.flush(a.out, lane);
 }
 
 // --------------------------------------------------------------- planning
@@ -431,8 +595,27 @@ static int engine_blocks() {
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine<PullSegs>, kThreads, 0));
     if (per_sm < 1) per_sm = 1;
     blocks = per_sm * sm_count();
+    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
+    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PushSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
   }
   return blocks;
+}
+
+// Owner costs split by tier: cs (warp tier) / cb (block tier), relative to x0.
+__global__ void k_split_cost(const int64_t* __restrict__ cp, int64_t x0, int64_t x1,
+                             const int32_t* __restrict__ owner_map, const int64_t* __restrict__ tab_indptr,
+                             int warp_cap, int64_t* cs, int64_t* cb) {
+  GRID_STRIDE(i, x1 - x0 + 1) {
+    int64_t x = x0 + i;
+    int64_t c = 0, d = 0;
+    if (x < x1) {
+      c = cp[x + 1] - cp[x];
+      int64_t u = owner_map ? (int64_t)owner_map[x] : x;
+      d = tab_indptr[u + 1] - tab_indptr[u];
+    }
+    cs[i] = (d <= warp_cap) ? c : 0;
+    cb[i] = (d > warp_cap) ? c : 0;
+  }
 }
 
 template <class Segs>
@@ -440,17 +623,41 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
                 const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
                 const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
                 cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
-  int blocks = engine_blocks();
-  int nW = blocks * kWarps;
-  int nmax = 10 * nW + 8;
-  int64_t* chunk_r = sc.alloc<int64_t>(nmax + 1);
-  int32_t* chunk_x = sc.alloc<int32_t>(nmax);
-  int* ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
-  TC_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
-  k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(cp, row_indptr, x0, x1, nW, nmax, chunk_r, chunk_x, ctl, mode);
+  const int blocks = engine_blocks();
+  const int big_blocks = sm_count();
+  const int64_t nx = x1 - x0;
+  // tier cost prefixes (relative to x0; the planner indexes them by owner id)
+  int64_t* cs = sc.alloc<int64_t>(nx + 1);
+  int64_t* cb = sc.alloc<int64_t>(nx + 1);
+  int64_t* ps = sc.alloc<int64_t>(nx + 1);
+  int64_t* pb = sc.alloc<int64_t>(nx + 1);
+  k_split_cost<<<grid_for(nx + 1, 256, sm_count() * 16), 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr,
+                                                                      g_warp_cap, cs, cb);
   check_launch();
-  EngineArgs a{row_indptr, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
-               bucket_bounds, nbuckets, out, n_owner, owner_map};
+  {
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cs, ps, nx + 1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cs, ps, nx + 1, s));
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cb, pb, nx + 1, s));
+  }
+  struct Tier { int workers; int64_t* chunk_r; int32_t* chunk_x; int* ctl; int nmax; const int64_t* cp; };
+  Tier tiers[2];
+  const int workers[2] = {blocks * kWarps, big_blocks};
+  const int64_t* cps[2] = {ps - x0, pb - x0};
+  for (int k = 0; k < 2; ++k) {
+    Tier& T = tiers[k];
+    T.workers = workers[k];
+    T.nmax = 10 * T.workers + 8;
+    T.chunk_r = sc.alloc<int64_t>(T.nmax + 1);
+    T.chunk_x = sc.alloc<int32_t>(T.nmax);
+    T.ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
+    T.cp = cps[k];
+    TC_CUDA(cudaMemsetAsync(T.ctl, 0, 2 * sizeof(int), s));
+    k_plan<<<grid_for(T.nmax + 1, 256), 256, 0, s>>>(T.cp, row_indptr, x0, x1, T.workers, T.nmax, T.chunk_r,
+                                                     T.chunk_x, T.ctl, mode);
+    check_launch();
+  }
   if (g_time_engine) {
     if (!g_ev[0]) {
       TC_CUDA(cudaEventCreate(&g_ev[0]));
@@ -458,7 +665,13 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
     }
     TC_CUDA(cudaEventRecord(g_ev[0], s));
   }
-  k_engine<Segs><<<blocks, kThreads, 0, s>>>(a, segs);
+  EngineArgs a0{row_indptr, tab_indptr, tab_indices, pool, tiers[0].chunk_r, tiers[0].chunk_x, tiers[0].ctl,
+                tiers[0].ctl + 1, bucket_bounds, nbuckets, out, n_owner, owner_map, g_warp_cap, g_big_cap};
+  k_engine<Segs><<<blocks, kThreads, 0, s>>>(a0, segs);
+  check_launch();
+  EngineArgs a1{row_indptr, tab_indptr, tab_indices, pool, tiers[1].chunk_r, tiers[1].chunk_x, tiers[1].ctl,
+                tiers[1].ctl + 1, bucket_bounds, nbuckets, out, n_owner, owner_map, g_warp_cap, g_big_cap};
+  k_engine_big<Segs><<<big_blocks, kBigThreads, kBigSmem, s>>>(a1, segs);
   check_launch();
   if (g_time_engine) {
     TC_CUDA(cudaEventRecord(g_ev[1], s));
@@ -607,6 +820,20 @@ int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_
       tcb::g_time_engine = enable != 0;
       tcb::g_engine_ms = 0.0;
       tcb::g_engine_launches = 0;
+    }
+  });
+}
+
+int tc_set_tuning(int32_t key, int64_t value) {
+  return tcb::guarded([&] {
+    if (key == 0) {
+      TC_REQUIRE(value >= 0 && value <= tcb::kTabCap, TC_EINVAL, "warp cap out of range");
+      tcb::g_warp_cap = (int)value;
+    } else if (key == 1) {
+      TC_REQUIRE(value >= 0 && value <= tcb::kBigCap, TC_EINVAL, "block cap out of range");
+      tcb::g_big_cap = (int)value;
+    } else {
+      throw tcb::Error(TC_EINVAL, "unknown tuning key");
     }
   });
 }

@@ -298,3 +298,46 @@ def test_rmat_scale_properties():
     same_row = src[1:] == src[:-1]
     assert np.all(ix[1:][same_row] > ix[:-1][same_row])
     assert int(g.deg.sum()) == 2 * g.m
+
+
+@pytest.mark.parametrize("caps", [(0, 4096), (8, 4096), (8, 8), (0, 0)])
+def test_engine_tiers_forced(caps):
+    """Force owners through the block tier (warp cap lowered) and through
+    the global-memory fallback (block cap lowered); results must not move."""
+    from paper_1406_5687_b200 import _lib
+    L = _lib.lib()
+    cases = ["pa_2000_10_3", "rmat_s10", "sparse_labels", "er_150_0.5_5", "gnm_2000_16000"]
+    try:
+        _lib.check(L.tc_set_tuning(0, caps[0]))
+        _lib.check(L.tc_set_tuning(1, caps[1]))
+        for name in cases:
+            case = SMALL[name]
+            _, g = graph_of(name)
+            T = int(case["T"][0])
+            assert tcb.count_triangles_seq(g) == T, name
+            assert int(count_lowest(g).item()) == T, name
+            total, rr = tcb.count_space_surrogate(g, 3)
+            assert [m.triangles for m in rr.metrics] == case["surr_tri_3"].tolist(), name
+            b = torch.as_tensor(case["bounds_predsum_5"]).cuda()
+            assert host(count_lowest(g, 0, g.n, bounds=b)).tolist() == case["lowest_5"].tolist(), name
+    finally:
+        L.tc_set_tuning(0, 256)
+        L.tc_set_tuning(1, 4096)
+
+
+def test_dense_core_block_tier():
+    """A dense core (K_320 plus random edges) puts d^ > 256 tables on the
+    block tier at default caps; checked against the oracle."""
+    rng = np.random.default_rng(5)
+    core = np.array([(a, b) for a in range(320) for b in range(a + 1, 320)], np.int64)
+    extra = rng.integers(0, 3000, size=(20000, 2))
+    raw = np.concatenate([core, extra])
+    og = O.build_graph(*O.normalize(raw))
+    assert int(og.eff_deg.max()) > 256
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(raw)))
+    T = O.count_triangles(og)
+    assert tcb.count_triangles_seq(g) == T
+    assert int(count_lowest(g).item()) == T
+    partials, census = O.surrogate(og, O.balanced_bounds(O.node_costs(og, "predsum"), 0, og.n, 4))
+    total, rr = tcb.count_space_surrogate(g, 4)
+    assert [m.triangles for m in rr.metrics] == partials.tolist()
