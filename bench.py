@@ -45,6 +45,11 @@ CONFIGS = {
     "cfg2": dict(kind="pa", n=1_000_000, d=100, seed=1,
                  desc="cfg2 BA/PA n=1,000,000 d=100 (50 distinct degree-proportional targets) seed=1 "
                       "(reference generate_pa, bit-identical)"),
+    "cfg3": dict(kind="cl", n=4_000_000, mean=80.0, gamma=2.1, wmax=200_000.0, seed=1,
+                 desc="cfg3 Chung-Lu n=4,000,000 gamma=2.1 mean=80 w_max=200,000, exact p_uv model, seed=1 "
+                      "(device generator)"),
+    "cfg4": dict(kind="rmat", scale=24, ef=32, seed=1,
+                 desc="cfg4 R-MAT scale 24 edge factor 32 (.57,.19,.19,.05) seed=1, no permutation (device generator)"),
     "cfg4s20": dict(kind="rmat", scale=20, ef=32, seed=1,
                     desc="R-MAT scale 20 edge factor 32 (.57,.19,.19,.05) seed=1 (cfg4 family, reduced scale)"),
     "cfg5": dict(kind="er", n=2_000_000, m=400_000_000, seed=1,
@@ -131,7 +136,13 @@ def host_raw_edges(cfg, pin):
     c = CONFIGS[cfg]
     if c["kind"] == "pa":
         return pa_edges_host(tcb.PaParams(c["n"], c["d"], c["seed"]), pin=pin)
-    dev = er_edges(c["n"], c["m"], c["seed"]) if c["kind"] == "er" else rmat_edges(c["scale"], c["ef"], c["seed"])
+    if c["kind"] == "er":
+        dev = er_edges(c["n"], c["m"], c["seed"])
+    elif c["kind"] == "cl":
+        from paper_1406_5687_b200.graph_io import chung_lu_edges
+        dev = chung_lu_edges(c["n"], c["mean"], c["gamma"], c["wmax"], c["seed"])
+    else:
+        dev = rmat_edges(c["scale"], c["ef"], c["seed"])
     out = torch.empty(tuple(dev.shape), dtype=torch.int32, pin_memory=pin)
     out.copy_(dev)
     del dev
@@ -139,11 +150,14 @@ def host_raw_edges(cfg, pin):
 
 
 def oracle_raw_edges(cfg):
-    """Reference-arm input: built without any product kernel."""
+    """Reference-arm input: built without any product kernel (Chung-Lu, which
+    has no host twin, is generated on the device like the GPU arm's)."""
     from oracle import gen_twin
     from oracle import oracle as O
 
     c = CONFIGS[cfg]
+    if c["kind"] == "cl":
+        return host_raw_edges(cfg, pin=False).numpy().astype(np.int64)
     if c["kind"] == "pa":
         return O.pa_edge_list(c["n"], c["d"], c["seed"])
     if c["kind"] == "er":

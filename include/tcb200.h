@@ -180,10 +180,12 @@ int tc_surrogate_census(const int64_t* eff_indptr, const int32_t* eff_indices, i
 /* Owner-change records of one rank (the send list of the surrogate push):
  * for owned v in [bounds[rank], bounds[rank+1]) emits one (v, dest) per
  * remote rank dest > rank touched by N^_v, grouped by dest ascending then v
- * ascending.  rec_v/rec_dest int32[cap]; counts int64[P] per dest.
+ * ascending.  The CSR row of global node v is eff_indptr[v - row_base]
+ * (row_base = 0 for a whole graph, = bounds[rank] for a rank's shard).
+ * rec_v/rec_dest int32[cap]; counts int64[P] per dest.
  * Synchronises (returns the record count). */
 int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n,
-                         const int64_t* bounds, int32_t P, int32_t rank, int32_t* rec_v,
+                         const int64_t* bounds, int32_t P, int32_t rank, int64_t row_base, int32_t* rec_v,
                          int32_t* rec_dest, int64_t cap, long long* counts,
                          int64_t* nrec_host, tc_stream_t stream);
 
@@ -222,6 +224,13 @@ int tc_gen_er(int64_t n, int64_t m, uint64_t seed, int32_t* out, tc_stream_t str
 /* R-MAT raw pairs (config 4): 2^scale*edge_factor samples, (.57,.19,.19,.05). */
 int tc_gen_rmat(int32_t scale, int64_t edge_factor, uint64_t seed, int32_t* out,
                 tc_stream_t stream);
+/* Chung-Lu raw pairs (config 3), exact model: w_i = c (i+1)^(-1/(gamma-1))
+ * capped at w_max and scaled to mean degree `mean`; every pair u < v is an
+ * edge independently with p_uv = min(1, w_u w_v / sum w) (geometric-skip
+ * sampling per row).  out == NULL returns the edge count only; otherwise
+ * out int32[2*cap].  Synchronises (returns m). */
+int tc_gen_chung_lu(int64_t n, double mean, double gamma, double w_max, uint64_t seed, int32_t* out,
+                    int64_t cap, int64_t* m_host, tc_stream_t stream);
 /* Preferential attachment, bit-identical to the reference's pa_edge_list
  * (_kernels.py:129-178; sequential by construction, runs on the host).
  * out_host int32[2*tc_pa_num_edges(n,k)] as (src, dst) pairs. */

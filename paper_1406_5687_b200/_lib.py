@@ -40,13 +40,14 @@ _SIGS = {
     "tc_balanced_bounds": [_vp, _i64, _i64, _i64, _vp, _vp],
     "tc_plan_tasks": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _pi64, _vp],
     "tc_surrogate_census": [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
-    "tc_surrogate_records": [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _vp, _i64, _vp, _pi64, _vp],
+    "tc_surrogate_records": [_vp, _vp, _i64, _vp, _i32, _i32, _i64, _vp, _vp, _i64, _vp, _pi64, _vp],
     "tc_surrogate_pack_sizes": [_vp, _vp, _i64, _vp, _pi64, _vp],
     "tc_surrogate_pack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_owner_segments": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _pi64, _vp],
     "tc_segments_csr": [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "tc_gen_er": [_i64, _i64, _u64, _vp, _vp],
     "tc_gen_rmat": [_i32, _i64, _u64, _vp, _vp],
+    "tc_gen_chung_lu": [_i64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _u64, _vp, _i64, _pi64, _vp],
     "tc_pa_num_edges": [_i64, _i64],
     "tc_gen_pa_host": [_i64, _i64, _u64, _vp],
 }

@@ -198,11 +198,11 @@ __global__ void k_census(const int64_t* __restrict__ indptr, const int32_t* __re
 
 // number of records of each owned v (for the two-pass emit)
 __global__ void k_rec_count(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            const int64_t* __restrict__ bounds, int P, int rank, int32_t* cnt) {
+                            const int64_t* __restrict__ bounds, int P, int rank, int64_t row_base, int32_t* cnt) {
   const int64_t lo = bounds[rank], hi = bounds[rank + 1];
   GRID_STRIDE(i, hi - lo) {
     int64_t v = lo + i;
-    int64_t e0 = indptr[v], e1 = indptr[v + 1];
+    int64_t e0 = indptr[v - row_base], e1 = indptr[v - row_base + 1];
     int seg = rank, last = -1, c = 0;
     for (int64_t e = e0; e < e1; ++e) {
       int64_t u = indices[e];
@@ -217,12 +217,12 @@ __global__ void k_rec_count(const int64_t* __restrict__ indptr, const int32_t* _
 }
 
 __global__ void k_rec_emit(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                           const int64_t* __restrict__ bounds, int P, int rank,
+                           const int64_t* __restrict__ bounds, int P, int rank, int64_t row_base,
                            const int32_t* __restrict__ off, uint32_t* dest, int32_t* vv) {
   const int64_t lo = bounds[rank], hi = bounds[rank + 1];
   GRID_STRIDE(i, hi - lo) {
     int64_t v = lo + i;
-    int64_t e0 = indptr[v], e1 = indptr[v + 1];
+    int64_t e0 = indptr[v - row_base], e1 = indptr[v - row_base + 1];
     int seg = rank, last = -1;
     int64_t o = off[i];
     for (int64_t e = e0; e < e1; ++e) {
@@ -368,7 +368,7 @@ int tc_surrogate_census(const int64_t* eff_indptr, const int32_t* eff_indices, i
 }
 
 int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n,
-                         const int64_t* bounds, int32_t P, int32_t rank, int32_t* rec_v,
+                         const int64_t* bounds, int32_t P, int32_t rank, int64_t row_base, int32_t* rec_v,
                          int32_t* rec_dest, int64_t cap, long long* counts, int64_t* nrec_host,
                          tc_stream_t stream) {
   return tcb::guarded([&] {
@@ -386,7 +386,7 @@ int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, 
     int32_t* cnt = sc.alloc<int32_t>(nv + 1);
     int32_t* off = sc.alloc<int32_t>(nv + 1);
     TC_CUDA(cudaMemsetAsync(cnt + nv, 0, sizeof(int32_t), s));
-    tcb::k_rec_count<<<tcb::grid_for(nv, 256), 256, 0, s>>>(eff_indptr, eff_indices, bounds, P, rank, cnt);
+    tcb::k_rec_count<<<tcb::grid_for(nv, 256), 256, 0, s>>>(eff_indptr, eff_indices, bounds, P, rank, row_base, cnt);
     tcb::check_launch();
     tcb::exclusive_sum(sc, cnt, off, nv + 1, s);
     int32_t nrec = tcb::read_scalar(off + nv, s);
@@ -397,7 +397,7 @@ int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, 
     uint32_t* dk2 = sc.alloc<uint32_t>(nrec);
     int32_t* vv = sc.alloc<int32_t>(nrec);
     int32_t* vv2 = sc.alloc<int32_t>(nrec);
-    tcb::k_rec_emit<<<tcb::grid_for(nv, 256), 256, 0, s>>>(eff_indptr, eff_indices, bounds, P, rank, off, dk, vv);
+    tcb::k_rec_emit<<<tcb::grid_for(nv, 256), 256, 0, s>>>(eff_indptr, eff_indices, bounds, P, rank, row_base, off, dk, vv);
     tcb::check_launch();
     {  // stable sort by destination: grouped by dest, v ascending within
       cub::DoubleBuffer<uint32_t> k(dk, dk2);

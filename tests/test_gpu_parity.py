@@ -341,3 +341,32 @@ def test_dense_core_block_tier():
     partials, census = O.surrogate(og, O.balanced_bounds(O.node_costs(og, "predsum"), 0, og.n, 4))
     total, rr = tcb.count_space_surrogate(g, 4)
     assert [m.triangles for m in rr.metrics] == partials.tolist()
+
+
+@pytest.mark.parametrize("name", ["er_60_0.2_21", "pa_1500_12_3", "sparse_labels", "rmat_s10", "gnm_2000_16000", "k9"])
+def test_multi_rank_path_emulated(name):
+    """The per-rank device kernels of the multi-GPU surrogate protocol
+    (records, pack, owner segments, segment count), ranks run one after
+    another on one GPU and buffers passed directly: partials, census, bytes
+    and partition sizes equal the reference's count_space_surrogate."""
+    from paper_1406_5687_b200.distributed import emulate_ranks
+    case = SMALL[name]
+    _, g = graph_of(name)
+    for P in (2, 3, 5, 8):
+        total, mets = emulate_ranks(g, P)
+        assert total == int(case["T"][0])
+        assert [m.triangles for m in mets] == case[f"surr_tri_{P}"].tolist()
+        assert np.array_equal(np.stack([m.data_msgs_to for m in mets]), case[f"surr_census_{P}"])
+        assert [m.bytes_sent for m in mets] == case[f"surr_bytes_{P}"].tolist()
+        assert [m.partition_bytes for m in mets] == case[f"surr_pbytes_{P}"].tolist()
+
+
+def test_multi_rank_path_cfg1(configs):
+    from paper_1406_5687_b200.distributed import emulate_ranks
+    c = configs["cfg1_er_gnm_16384_131072_seed1"]
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=16384, edges=er_edges(16384, 131072, 1))))
+    for P in (2, 4, 8):
+        total, mets = emulate_ranks(g, P)
+        assert total == c["T"]
+        assert [m.triangles for m in mets] == c[f"surr_tri_{P}"]
+        assert np.stack([m.data_msgs_to for m in mets]).tolist() == c[f"surr_census_{P}"]
