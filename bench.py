@@ -244,6 +244,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
+    ap.add_argument("--mode", default="surrogate", choices=["surrogate", "replicated"],
+                    help="N>1: the paper's non-overlapping partition with list exchange, or replicated graph")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: --warmup < 3 is below the timing contract; using 3")
@@ -303,15 +305,26 @@ def _gpu_arm_core(args):
     n, m = g.n, g.m
     W = int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum())
 
-    if world > 1:
+    mode = args.mode if world > 1 else "single"
+    if mode == "replicated":
         ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
         ub = balanced_bounds(ucost, 0, n, world).cpu().numpy()
         u0, u1 = int(ub[rank]), int(ub[rank + 1])
     else:
         u0, u1 = 0, n
     out = torch.empty(1, dtype=torch.int64, device=dev)
+    if mode == "surrogate":
+        from paper_1406_5687_b200.distributed import shard_of, surrogate_rank
+        from paper_1406_5687_b200.partitioning import partition_ranges, range_bounds
+
+        sb = range_bounds(partition_ranges(g, tcb.CostKind.PRED_SUM, world))
+        shard = shard_of(g, int(sb[rank]), int(sb[rank + 1]))
 
     def count_step():
+        if mode == "surrogate":
+            total, _ = surrogate_rank(shard, sb)
+            out.fill_(total)
+            return out
         count_middle(g, u0, u1, out=out)
         if world > 1:
             dist.all_reduce(out)
@@ -326,6 +339,7 @@ def _gpu_arm_core(args):
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _lib.lib().tc_launch_count()
     with ClockSampler(local) as clocks:
         barrier()
         for i in range(args.steps):
@@ -334,6 +348,7 @@ def _gpu_arm_core(args):
             r = count_step()
             ends[i].record()
         barrier()
+    launches = int(_lib.lib().tc_launch_count() - launches0)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms = max_over_ranks(sum(step_ms) / len(step_ms))
     if int(r.item()) != T:
@@ -351,6 +366,8 @@ def _gpu_arm_core(args):
 
     e2e_ms = None
     if not args.no_e2e:
+        if mode == "surrogate":
+            del shard
         del g
         torch.cuda.empty_cache()
         samples = []
@@ -360,7 +377,9 @@ def _gpu_arm_core(args):
             s.record()
             dev_raw = raw_host.to(dev, non_blocking=True)
             gg = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=dev_raw)))
-            if world > 1:
+            if mode == "surrogate":
+                tri, _ = surrogate_rank(shard_of(gg, int(sb[rank]), int(sb[rank + 1])), sb)
+            elif world > 1:
                 c = count_middle(gg, u0, u1)
                 dist.all_reduce(c)
                 tri = int(c.item())
@@ -403,7 +422,10 @@ def _gpu_arm_core(args):
         "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw,
                    "triangles": T, "W_succsum": W,
                    "l2": "inputs > L2 (rev_seg 16 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
-                   "parallelism": f"middle-vertex ranges x{world}" + (" + NCCL all-reduce" if world > 1 else "")},
+                   "parallelism": {"single": "1 GPU",
+                                   "replicated": f"{world} GPUs, replicated graph, cost-balanced middle-vertex ranges + NCCL all-reduce",
+                                   "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
+                                                "(NCCL all-to-all) + NCCL all-reduce"}[mode]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_engine<PullSegs> (middle-vertex engine)",
@@ -414,7 +436,7 @@ def _gpu_arm_core(args):
             "value": m / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": m_raw * 8,
             "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
             "path": "pinned host raw pairs -> H2D -> normalize -> build_graph -> count_triangles_seq -> D2H"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": launches,
         "clocks": clock_summary,
     }
     return line

@@ -46,6 +46,9 @@ enum { TC_COST_UNIT = 0, TC_COST_DEGREE = 1, TC_COST_SUCC_SUM = 2, TC_COST_PRED_
 
 const char* tc_last_error(void);
 int tc_abi_version(void);
+/* Number of this library's kernels launched so far in the process (CUB's
+ * sort/scan kernels excluded).  Measurement only. */
+unsigned long long tc_launch_count(void);
 /* Releases pooled scratch back to the driver (between large jobs). */
 int tc_trim_pool(void);
 

@@ -51,7 +51,7 @@ _SIGS = {
     "tc_pa_num_edges": [_i64, _i64],
     "tc_gen_pa_host": [_i64, _i64, _u64, _vp],
 }
-EXPORTED = sorted(_SIGS) + ["tc_last_error"]
+EXPORTED = sorted(_SIGS) + ["tc_last_error", "tc_launch_count"]
 
 
 def build_library(force=False):
@@ -72,6 +72,8 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = _i64 if name == "tc_pa_num_edges" else ctypes.c_int
+        L.tc_launch_count.argtypes = []
+        L.tc_launch_count.restype = ctypes.c_ulonglong
         L.tc_last_error.argtypes = []
         L.tc_last_error.restype = ctypes.c_char_p
         _LIB = L

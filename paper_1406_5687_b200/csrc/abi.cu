@@ -6,6 +6,7 @@
 namespace tcb {
 
 static thread_local std::string g_last_error;
+unsigned long long g_launches = 0;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -34,6 +35,8 @@ extern "C" {
 const char* tc_last_error(void) { return tcb::g_last_error.c_str(); }
 
 int tc_abi_version(void) { return 1; }
+
+unsigned long long tc_launch_count(void) { return tcb::g_launches; }
 
 int tc_trim_pool(void) {
   return tcb::guarded([&] {

@@ -94,7 +94,14 @@ int sm_count();
 
 inline void sync_stream(cudaStream_t s) { TC_CUDA(cudaStreamSynchronize(s)); }
 
-inline void check_launch() { TC_CUDA(cudaGetLastError()); }
+// Counts launches of this library's own kernels (every launch site calls
+// check_launch); CUB's kernels are not counted.  Read by tc_launch_count.
+extern unsigned long long g_launches;
+
+inline void check_launch() {
+  ++g_launches;
+  TC_CUDA(cudaGetLastError());
+}
 
 }  // namespace tcb
 

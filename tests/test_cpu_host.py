@@ -18,7 +18,7 @@ from oracle import gen_twin
 
 def header_symbols():
     src = open(os.path.join(REPO, "include", "tcb200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|int)\s+(tc_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|unsigned long long|int64_t|int)\s+(tc_\w+)\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -370,3 +370,56 @@ def test_multi_rank_path_cfg1(configs):
         assert total == c["T"]
         assert [m.triangles for m in mets] == c[f"surr_tri_{P}"]
         assert np.stack([m.data_msgs_to for m in mets]).tolist() == c[f"surr_census_{P}"]
+
+
+def test_integration_stub_from_docs():
+    """The reference-side ctypes binding shown in INTEGRATION.md works as written."""
+    import os
+    import re
+    from conftest import REPO
+    src = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```python\n(.*?)```", src, re.S)
+    stub = [b for b in blocks if "tricount/_b200.py" in b][0]
+    stub = stub.replace("/path/to/paper_1406_5687_b200/libtcb200.so",
+                        os.path.join(REPO, "paper_1406_5687_b200", "libtcb200.so"))
+    ns = {}
+    exec(compile(stub, "INTEGRATION.md", "exec"), ns)
+    for name in ("er_40_0.3_11", "pa_2000_10_3", "sparse_labels"):
+        case = SMALL[name]
+        assert ns["count_triangles"](case["raw"]) == int(case["T"][0])
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5", "cfg4"])
+def test_full_scale_configs(cfg):
+    """Configs 3-5 at full BASELINE size, bit-exact against the pinned CPU
+    oracle run on the same device-generated edges (tests/golden/scale.json,
+    made by tests/golden/make_scale_golden.py): raw-pair checksum, n, m, the
+    relabel / CSR checksums, W and the triangle total (both engines)."""
+    import json
+    import os
+    from conftest import GOLDEN
+    import bench
+    want = json.load(open(os.path.join(GOLDEN, "scale.json")))[cfg]
+    c = bench.CONFIGS[cfg]
+    if c["kind"] == "er":
+        raw = er_edges(c["n"], c["m"], c["seed"])
+    elif c["kind"] == "rmat":
+        raw = rmat_edges(c["scale"], c["ef"], c["seed"])
+    else:
+        from paper_1406_5687_b200.graph_io import chung_lu_edges
+        raw = chung_lu_edges(c["n"], c["mean"], c["gamma"], c["wmax"], c["seed"])
+    assert raw.shape[0] == want["raw_pairs"]
+    assert gen_twin.checksum(raw.cpu().numpy()) == want["raw_checksum"]
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw)))
+    del raw
+    assert (g.n, g.m) == (want["n"], want["m"])
+    assert gen_twin.checksum(g.relabel.cpu().numpy()) == want["relabel_checksum"]
+    assert gen_twin.checksum(g.eff_indptr.cpu().numpy()) == want["eff_indptr_checksum"]
+    assert gen_twin.checksum(g.eff_indices.cpu().numpy()) == want["eff_indices_checksum"]
+    assert int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum()) == want["W"]
+    assert tcb.count_triangles_seq(g) == want["T"]
+    assert int(count_lowest(g).item()) == want["T"]
+    total, rr = tcb.count_space_surrogate(g, 8)
+    assert total == want["T"]
+    del g
+    torch.cuda.empty_cache()
