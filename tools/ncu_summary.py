@@ -32,7 +32,8 @@ if len(sys.argv) > 2:
     rows = list(csv.reader(io.StringIO(src)))
     hdr = rows[1]
     ia, ss, sc = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
-    data = [(r[sc], int(r[ia] or 0), int(r[ss] or 0)) for r in rows[2:] if len(r) > ia]
+    end = next((i for i in range(2, len(rows)) if rows[i] and rows[i][0] == "Kernel Name"), len(rows))
+    data = [(r[sc], int(r[ia] or 0), int(r[ss] or 0)) for r in rows[2:end] if len(r) > ia and (r[ia] or "0").isdigit()]
     blocks = []
     for s_, c, smp in data:
         if blocks and blocks[-1][0] == c:
