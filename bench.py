@@ -355,13 +355,14 @@ def _gpu_arm_core(args):
         raise RuntimeError("count changed between steps")
 
     # dominant kernel (the engine) timed with CUDA events on its own stream
-    _lib.lib().tc_engine_timing(1, None, None)
+    _lib.lib().tc_engine_timing(1, None, None, None)
     for _ in range(args.steps):
         flush.fill_(1)
         count_step()
     torch.cuda.synchronize()
     tot, nl = ctypes.c_double(), ctypes.c_longlong()
-    _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl))
+    tiers = (ctypes.c_double * 3)()
+    _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl), tiers)
     engine_ms = max_over_ranks(tot.value / max(1, nl.value))
 
     e2e_ms = None

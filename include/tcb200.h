@@ -134,14 +134,17 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
                     unsigned long long* out, tc_stream_t stream);
 
 /* Engine timing (measurement only): reports the accumulated device time and
- * launch count of engine kernels since the last reset, then, if enable >= 0,
- * resets the counters and turns CUDA-event bracketing of every engine
- * launch on (1) or off (0).  Bracketing synchronises after each launch. */
-int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host);
+ * launch count of engine kernels since the last reset (tier_ms_host, if not
+ * NULL, gets the time of the small / mid / block tiers), then, if
+ * enable >= 0, resets the counters and turns CUDA-event bracketing of every
+ * engine launch on (1) or off (0).  Bracketing synchronises after each
+ * launch. */
+int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host, double* tier_ms_host);
 
-/* Engine tier caps (testing / tuning): key 0 = warp-tier table cap
- * (0..256, default 256), key 1 = block-tier staged-table cap (0..4096,
- * default 4096; larger tables use binary search in global memory). */
+/* Engine tier caps (testing / tuning): key 0 = small warp-tier table cap
+ * (0..256, default 256), key 2 = mid warp-tier cap (0..1024, default 1024),
+ * key 1 = block-tier staged-table cap (0..4096, default 4096; larger tables
+ * use binary search in global memory). */
 int tc_set_tuning(int32_t key, int64_t value);
 
 /* |a ∩ b| of two strictly ascending int32 lists (_kernels.py:15-37). */

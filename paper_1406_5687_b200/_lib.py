@@ -33,7 +33,7 @@ _SIGS = {
     "tc_count_owners": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp],
     "tc_tile_pull": [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "tc_intersect_count": [_vp, _i64, _vp, _i64, _vp, _vp],
-    "tc_engine_timing": [_i32, _vp, _vp],
+    "tc_engine_timing": [_i32, _vp, _vp, _vp],
     "tc_set_tuning": [_i32, _i64],
     "tc_count_brute": [_vp, _vp, _i64, _vp, _vp],
     "tc_node_costs": [_i32, _vp, _vp, _vp, _vp, _i64, _vp, _vp],

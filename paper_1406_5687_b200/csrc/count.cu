@@ -40,16 +40,21 @@
 namespace tcb {
 
 #ifndef TCB_MINBLOCKS
-#define TCB_MINBLOCKS 6
+#define TCB_MINBLOCKS 5
 #endif
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
-static constexpr int kWarps = 8;          // warps per block (warp tier)
+static constexpr int kWarps = 8;          // warps per block (small tier)
 static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
-static constexpr int kTabCap = 256;       // warp tier: ids per table (sorted copy)
-static constexpr int kLwWarp = 9;         // warp tier filter: 2^9 words = 16K bits (2 KB)
+static constexpr int kTabCap = 256;       // small tier: ids per table
+static constexpr int kLwWarp = 9;         // small tier filter: 2^9 words = 16K bits (2 KB)
+static constexpr int kLbWarp = 7;         // small tier buckets: 2^7 x 4 ids (2 KB), load <= 1/2
+static constexpr int kMidCap = 512;       // mid tier: ids per table
+static constexpr int kLwMid = 10;         // mid tier filter: 2^10 words = 32K bits (4 KB)
+static constexpr int kLbMid = 8;          // mid tier buckets: 2^8 x 4 ids (4 KB), load <= 1/2
+static constexpr int kMidWarps = 4;       // mid tier: warps per block (8 KB private slices)
 static constexpr int kBigThreads = 512;   // block tier
 static constexpr int kBigWarps = kBigThreads / 32;
 static constexpr int kBigCap = 4096;      // block tier: ids per staged table
@@ -64,11 +69,12 @@ static constexpr int kTabCost = 16;
 static constexpr int32_t kEmpty = -1;
 
 // Verification kinds of a staged table (see probe4).
-enum : int { kGlobal = 0, kSorted = 1, kBuckets = 2 };
+enum : int { kGlobal = 0, kInline = 1, kBuckets = 2 };
 
-struct WarpSlice {
-  int32_t tab[kTabCap];
-  uint32_t bm[1 << kLwWarp];
+template <int kLb, int kLw>
+struct WarpSliceT {
+  uint32_t bm[1 << kLw];
+  int4 bkt[1 << kLb];
 };
 
 // --------------------------------------------------------------- segments
@@ -96,8 +102,9 @@ struct PushSegs {  // forward edge e of v -> N^_u, u = indices[e]
 // front (2^lw words, h = id * golden, word = h >> (32 - lw), bit =
 // (h >> (27 - lw)) & 31): a probe is one LDS.32 and three ALU ops, and only
 // filter hits (true hits plus ~d/2^(lw+5) false positives) are verified:
-//   kSorted  (warp tier): binary search in a sorted shared copy, inline --
-//            cheapest when hits are rare (PA: 0.4% of probes);
+//   kInline  (warp tiers): inline lookup in a bucketized hash table whose
+//            maximum displacement is recorded at build time, so a lookup is a
+//            warp-uniform handful of LDS.128 (usually one), no search loop;
 //   kBuckets (block tier): hits are queued per warp and verified in bulk
 //            against a bucketized hash table (2^lb buckets of 4 ids,
 //            bucket = h >> (32 - lb), overflow to the next bucket, load
@@ -113,10 +120,18 @@ __device__ __forceinline__ int tab_lb(int64_t d) {  // log2 buckets: smallest 2^
   return max(lb, 3);
 }
 
+// One bit per id: word = top lw hash bits, bit = the next 5.  (A blocked
+// Bloom variant with two bits per id in the same word was measured: -4% on
+// cfg 2, +3% on cfg 5 -- not worth the extra ALU.)
+template <int kLw>
+__device__ __forceinline__ uint32_t filt_mask(uint32_t h) {
+  return 1u << ((h >> (27 - kLw)) & 31);
+}
+
 template <int kLw>
 __device__ __forceinline__ void filt_insert(uint32_t* bm, int32_t w) {
   const uint32_t h = tab_hash((uint32_t)w);
-  atomicOr(&bm[h >> (32 - kLw)], 1u << ((h >> (27 - kLw)) & 31));
+  atomicOr(&bm[h >> (32 - kLw)], filt_mask<kLw>(h));
 }
 
 template <int kLw>
@@ -124,19 +139,31 @@ __device__ __forceinline__ void filt_clear(uint32_t* bm, int32_t w) {
   bm[tab_hash((uint32_t)w) >> (32 - kLw)] = 0;
 }
 
-__device__ __forceinline__ void bkt_insert(int4* bkt, int lb, int32_t w) {
+__device__ __forceinline__ bool bkt_has(int4 q, int32_t x) { return (q.x == x) | (q.y == x) | (q.z == x) | (q.w == x); }
+
+// Inserts w; returns its displacement (buckets past its home bucket).
+__device__ __forceinline__ int bkt_insert(int4* bkt, int lb, int32_t w) {
   int32_t* slots = reinterpret_cast<int32_t*>(bkt);
   const uint32_t mask = (1u << lb) - 1;
   uint32_t b = tab_hash((uint32_t)w) >> (32 - lb);
-  for (;;) {
+  for (int i = 0;; ++i) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (atomicCAS(&slots[b * 4 + k], kEmpty, w) == kEmpty) return;
+      if (atomicCAS(&slots[b * 4 + k], kEmpty, w) == kEmpty) return i;
     b = (b + 1) & mask;
   }
 }
 
-__device__ __forceinline__ bool bkt_has(int4 q, int32_t x) { return (q.x == x) | (q.y == x) | (q.z == x) | (q.w == x); }
+// Membership with a known maximum displacement (warp-uniform per table):
+// a fixed number of bucket reads, no data-dependent loop.
+__device__ __forceinline__ bool bkt_find(const int4* bkt, int lb, int dmax, int32_t x) {
+  const uint32_t mask = (1u << lb) - 1;
+  const uint32_t b = tab_hash((uint32_t)x) >> (32 - lb);
+  bool f = bkt_has(bkt[b], x);
+  for (int i = 1; i <= dmax; ++i) f |= bkt_has(bkt[(b + i) & mask], x);
+  return f;
+}
+
 
 __device__ __forceinline__ bool bkt_lookup(const int4* bkt, int lb, int32_t x) {
   const uint32_t mask = (1u << lb) - 1;
@@ -170,13 +197,14 @@ __device__ __forceinline__ bool bsearch_gmem(const int32_t* __restrict__ t, int6
 }
 
 struct Table {
-  const uint32_t* bm;   // filter (kSorted, kBuckets)
-  const int32_t* tab;   // sorted shared copy (kSorted) or global list (kGlobal)
-  const int4* bkt;      // buckets (kBuckets)
+  const uint32_t* bm;   // filter (kInline, kBuckets)
+  const int32_t* tab;   // global list (kGlobal)
+  const int4* bkt;      // buckets (kInline, kBuckets)
   int32_t* pos;         // per-warp hit queue (kBuckets)
   int64_t d;
   int lb;
   int32_t tmin, tmax;
+  int dmax;             // max bucket displacement (kInline)
 };
 
 // Verify the queued filter hits of this warp (kBuckets) and empty the queue.
@@ -187,7 +215,10 @@ __device__ __forceinline__ void drain(const Table& t, int& npos, int lane, uint3
   npos = 0;
 }
 
-template <int kKind, int kLw>
+// Filter the 4 ids of v; `vmask` marks the ids inside the chunk's segment
+// (ids outside it belong to neighbouring lists and must not be counted).
+// Only filter hits are verified; no range check is needed for exactness.
+template <int kKind, int kLw, int kCap = kTabCap>
 __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, int lane, int& npos, uint32_t& cnt) {
   int32_t xs[4] = {v.x, v.y, v.z, v.w};
   if (kKind == kGlobal) {
@@ -200,15 +231,15 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t h = tab_hash((uint32_t)xs[k]);
-    const uint32_t bit = (t.bm[h >> (32 - kLw)] >> ((h >> (27 - kLw)) & 31)) & 1u;
-    const bool in = ((vmask >> k) & 1u) && xs[k] >= t.tmin && xs[k] <= t.tmax;
-    m |= (in ? bit : 0u) << k;
+    const uint32_t mk = filt_mask<kLw>(h);
+    m |= ((t.bm[h >> (32 - kLw)] & mk) == mk ? 1u : 0u) << k;
   }
-  if (kKind == kSorted) {
+  m &= vmask;
+  if (kKind == kInline) {
     if (m) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if ((m >> k) & 1u) cnt += bsearch_smem(t.tab, (int)t.d, xs[k]);
+        if ((m >> k) & 1u) cnt += bkt_find(t.bkt, t.lb, t.dmax, xs[k]);
     }
     return;
   }
@@ -235,17 +266,17 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 // Segment s covers chunks [excl_s, endx_s) of the flat space; chunk f of it
 // is pool4[delta_s + f]; `edge_s` packs (first-chunk offset | last-chunk
 // count << 2).
-template <int kKind, int kLw>
+template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                             int endx, int edge, int64_t delta, int total, int lane,
                                             int& npos, uint32_t& cnt) {
   const unsigned FULL = 0xffffffffu;
   const bool lane_seg = lane < nseg;
-  for (int base = 0; base < total; base += 32 * kWin) {
-    int4 v[kWin];
-    uint32_t vm[kWin];
+  for (int base = 0; base < total; base += 32 * kW) {
+    int4 v[kW];
+    uint32_t vm[kW];
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) {
+    for (int k = 0; k < kW; ++k) {
       const int b = base + 32 * k;
       vm[k] = 0;
       v[k] = make_int4(0, 0, 0, 0);
@@ -269,13 +300,13 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
       }
     }
 #pragma unroll
-    for (int k = 0; k < kWin; ++k) probe4<kKind, kLw>(t, v[k], vm[k], lane, npos, cnt);
+    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
     if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
   }
 }
 
 // One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner.
-template <int kKind, int kLw, class Segs>
+template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt) {
   const unsigned FULL = 0xffffffffu;
@@ -299,8 +330,8 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   }
   const int total = __shfl_sync(FULL, incl, 31);
   const int excl = incl - nch;
-  probe_group<kKind, kLw>(reinterpret_cast<const int4*>(pool), t, nseg, excl, incl, edge, c0s - excl, total, lane,
-                          npos, cnt);
+  probe_group<kKind, kLw, kCap, kW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, incl, edge, c0s - excl,
+                                    total, lane, npos, cnt);
 }
 
 struct EngineArgs {
@@ -316,13 +347,33 @@ struct EngineArgs {
   int nbuckets;
   unsigned long long* out;
   int64_t n_owner;            // row_indptr has n_owner + 1 entries
-  const int32_t* owner_map;   // nullable: owner x -> table/bucket node id
-  int warp_cap;               // tables with d <= warp_cap use the warp tier
+  const int32_t* owner_map;   // nullable: owner -> table/bucket node id
+  int64_t d_lo, d_hi;         // this launch handles owners with d_lo < d <= d_hi
   int big_cap;                // block tier stages d <= big_cap, else global search
+  // Tier compaction: the launch walks a compacted list of its own owners.
+  // x is a tier-local index; tier_owner[x] is the owner and its segments
+  // [row_indptr[x], row_indptr[x+1]) are physical [phys_row[o], ...).
+  const int32_t* tier_owner;
+  const int64_t* phys_row;
 };
+
+struct OwnerRef {
+  int64_t u;        // table / bucket node id
+  int64_t seg_off;  // physical segment index - tier-local segment index
+};
+
+__device__ __forceinline__ OwnerRef resolve_owner(const EngineArgs& a, int64_t x) {
+  int64_t o = x, off = 0;
+  if (a.tier_owner) {
+    o = __ldg(&a.tier_owner[x]);
+    off = __ldg(&a.phys_row[o]) - __ldg(&a.row_indptr[x]);
+  }
+  return OwnerRef{a.owner_map ? (int64_t)__ldg(&a.owner_map[o]) : o, off};
+}
 
 // Runtime tier caps (tc_set_tuning; tests lower them to force every tier).
 static int g_warp_cap = kTabCap;
+static int g_mid_cap = kMidCap;
 static int g_big_cap = kBigCap;
 
 __device__ __forceinline__ int bucket_of(const int64_t* bb, int nb, int64_t x) {
@@ -372,15 +423,16 @@ struct Acc {
   }
 };
 
-// Warp tier: owners with d <= kTabCap (larger ones belong to k_engine_big).
-template <class Segs>
-__global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a, Segs segs) {
-  __shared__ WarpSlice slices[kWarps];
+// Warp tiers (small: d <= 256 in 3 KB slices, 8 warps/block; mid:
+// d <= 1024 in 8 KB slices, 4 warps/block): each warp owns a private slice.
+template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW>
+__global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
+  __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
   const int lane = threadIdx.x & 31;
-  WarpSlice& sl = slices[threadIdx.x >> 5];
+  WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
-  for (int i = lane; i < (1 << kLwWarp); i += 32) sl.bm[i] = 0;
+  for (int i = lane; i < (1 << kLw); i += 32) sl.bm[i] = 0;
   __syncwarp();
   Acc acc;
 
@@ -398,24 +450,31 @@ __global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a
       const int64_t rb = min(xe_row, r1);
       const int64_t ra = r;
       r = rb;
-      const int64_t u = a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x;
+      const OwnerRef ow = resolve_owner(a, x);
+      const int64_t u = ow.u;
       const int64_t t0 = __ldg(&a.tab_indptr[u]);
       const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d <= 0 || d > a.warp_cap) continue;
+      if (d <= a.d_lo || d > a.d_hi) continue;
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + t0;
+      const int lb = min(tab_lb(d), kLb);
+      for (int i = lane; i < (1 << lb); i += 32) sl.bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
+      __syncwarp();
+      int disp = 0;
       for (int i = lane; i < d; i += 32) {
         const int32_t w = __ldg(&gtab[i]);
-        sl.tab[i] = w;
-        filt_insert<kLwWarp>(sl.bm, w);
+        filt_insert<kLw>(sl.bm, w);
+        disp = max(disp, bkt_insert(sl.bkt, lb, w));
       }
+      disp = __reduce_max_sync(FULL, disp);
+      Table t{sl.bm, nullptr, sl.bkt, nullptr, d, lb, 0, 0, disp};
       __syncwarp();
-      Table t{sl.bm, sl.tab, nullptr, nullptr, d, 0, sl.tab[0], sl.tab[d - 1]};
       int npos = 0;
       for (int64_t g = ra; g < rb; g += 32)
-        stream_group<kSorted, kLwWarp>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+        stream_group<kInline, kLw, Segs, kTabCap, kW>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
+                                                      lane, npos, acc.cnt);
       __syncwarp();
-      for (int i = lane; i < d; i += 32) filt_clear<kLwWarp>(sl.bm, sl.tab[i]);
+      for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
       __syncwarp();
     }
     acc.fold();
@@ -423,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, TCB_MINBLOCKS) k_engine(EngineArgs a
   acc.flush(a.out, lane);
 }
 
-// Block tier: owners with d > kTabCap.  The block stages the owner's table
+// Block tier: owners with d > d_lo (the mid tier's cap).  The block stages the owner's table
 // once per chunk-owner and its 16 warps stream groups of 32 segments.
 template <class Segs>
 __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Segs segs) {
@@ -456,10 +515,11 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
       const int64_t rb = min(xe_row, r1);
       const int64_t ra = r;
       r = rb;
-      const int64_t u = a.owner_map ? (int64_t)__ldg(&a.owner_map[x]) : x;
+      const OwnerRef ow = resolve_owner(a, x);
+      const int64_t u = ow.u;
       const int64_t t0 = __ldg(&a.tab_indptr[u]);
       const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d <= a.warp_cap) continue;
+      if (d <= a.d_lo) continue;
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + t0;
       const int lb = tab_lb(d);
@@ -482,13 +542,15 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
         Table t{bm, nullptr, bkt, pos, d, lb, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
         int npos = 0;
         for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kBuckets, kLwBig>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+          stream_group<kBuckets, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+                                         acc.cnt);
         drain(t, npos, lane, acc.cnt);
       } else {
         Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
         int npos = 0;
         for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kGlobal, 0>(segs, a.pool, t, g, min(g + 32, rb), lane, npos, acc.cnt);
+          stream_group<kGlobal, 0>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+                                   acc.cnt);
       }
     }
     acc.fold();
@@ -586,35 +648,75 @@ __global__ void k_push_cost(const int64_t* __restrict__ indptr, const int32_t* _
 static bool g_time_engine = false;
 static cudaEvent_t g_ev[2] = {nullptr, nullptr};
 static double g_engine_ms = 0.0;
+static double g_tier_ms[3] = {0.0, 0.0, 0.0};
+static cudaEvent_t g_tev[4] = {nullptr, nullptr, nullptr, nullptr};
 static long long g_engine_launches = 0;
 
-static int engine_blocks() {
-  static int blocks = 0;
-  if (!blocks) {
+// Engine tiers (same order as the cost split): small / mid warp tiers, block tier.
+#ifndef TCB_MID_WINDOWS
+#define TCB_MID_WINDOWS 4
+#endif
+#define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin>
+#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, 1, TCB_MID_WINDOWS>
+
+struct TierShape {
+  int blocks[3];   // persistent grid per tier
+  int workers[3];  // chunk-queue workers per tier (warps / warps / blocks)
+};
+
+static const TierShape& tier_shape() {
+  static TierShape ts;
+  static bool init = false;
+  if (!init) {
     int per_sm = 0;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine<PullSegs>, kThreads, 0));
-    if (per_sm < 1) per_sm = 1;
-    blocks = per_sm * sm_count();
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_SMALL(PullSegs), kThreads, 0));
+    ts.blocks[0] = std::max(per_sm, 1) * sm_count();
+    ts.workers[0] = ts.blocks[0] * kWarps;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_MID(PullSegs), kMidWarps * 32, 0));
+    ts.blocks[1] = std::max(per_sm, 1) * sm_count();
+    ts.workers[1] = ts.blocks[1] * kMidWarps;
     TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
     TC_CUDA(cudaFuncSetAttribute(k_engine_big<PushSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine_big<PullSegs>, kBigThreads, kBigSmem));
+    ts.blocks[2] = std::max(per_sm, 1) * sm_count();
+    ts.workers[2] = ts.blocks[2];
+    init = true;
   }
-  return blocks;
+  return ts;
 }
 
-// Owner costs split by tier: cs (warp tier) / cb (block tier), relative to x0.
-__global__ void k_split_cost(const int64_t* __restrict__ cp, int64_t x0, int64_t x1,
+// Tier of each owner in [x0, x1) (flags; owners without cost join no tier).
+__global__ void k_tier_flags(const int64_t* __restrict__ cp, int64_t x0, int64_t x1,
                              const int32_t* __restrict__ owner_map, const int64_t* __restrict__ tab_indptr,
-                             int warp_cap, int64_t* cs, int64_t* cb) {
+                             int c0, int c1, int32_t* f0, int32_t* f1, int32_t* f2) {
   GRID_STRIDE(i, x1 - x0 + 1) {
     int64_t x = x0 + i;
-    int64_t c = 0, d = 0;
-    if (x < x1) {
-      c = cp[x + 1] - cp[x];
+    int t = -1;
+    if (x < x1 && cp[x + 1] > cp[x]) {
       int64_t u = owner_map ? (int64_t)owner_map[x] : x;
-      d = tab_indptr[u + 1] - tab_indptr[u];
+      int64_t d = tab_indptr[u + 1] - tab_indptr[u];
+      t = (d <= c0) ? 0 : (d <= c1 ? 1 : 2);
     }
-    cs[i] = (d <= warp_cap) ? c : 0;
-    cb[i] = (d > warp_cap) ? c : 0;
+    f0[i] = t == 0;
+    f1[i] = t == 1;
+    f2[i] = t == 2;
+  }
+}
+
+// Compacts one tier: own[p] = owner, len[p] = its segment count, cost[p];
+// entries past the tier's size stay zero (caller memsets), so exclusive
+// scans over the full length give tier-local rows / cost prefixes.
+__global__ void k_tier_scatter(const int32_t* __restrict__ flag, const int32_t* __restrict__ pos, int64_t x0,
+                               int64_t nx, const int64_t* __restrict__ row_indptr, const int64_t* __restrict__ cp,
+                               int32_t* own, int64_t* len, int64_t* cost) {
+  GRID_STRIDE(i, nx) {
+    if (flag[i]) {
+      const int64_t x = x0 + i;
+      const int p = pos[i];
+      own[p] = (int32_t)x;
+      len[p] = row_indptr[x + 1] - row_indptr[x];
+      cost[p] = cp[x + 1] - cp[x];
+    }
   }
 }
 
@@ -623,40 +725,46 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
                 const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
                 const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
                 cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
-  const int blocks = engine_blocks();
-  const int big_blocks = sm_count();
+  (void)n_owner;
+  const TierShape& ts = tier_shape();
   const int64_t nx = x1 - x0;
-  // tier cost prefixes (relative to x0; the planner indexes them by owner id)
-  int64_t* cs = sc.alloc<int64_t>(nx + 1);
-  int64_t* cb = sc.alloc<int64_t>(nx + 1);
-  int64_t* ps = sc.alloc<int64_t>(nx + 1);
-  int64_t* pb = sc.alloc<int64_t>(nx + 1);
-  k_split_cost<<<grid_for(nx + 1, 256, sm_count() * 16), 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr,
-                                                                      g_warp_cap, cs, cb);
+  const int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
+  const int grid = grid_for(nx + 1, 256, sm_count() * 16);
+  int32_t* flag[3];
+  for (int k = 0; k < 3; ++k) flag[k] = sc.alloc<int32_t>(nx + 1);
+  k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2]);
   check_launch();
-  {
-    size_t tmp = 0;
-    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cs, ps, nx + 1, s));
-    void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cs, ps, nx + 1, s));
-    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cb, pb, nx + 1, s));
-  }
-  struct Tier { int workers; int64_t* chunk_r; int32_t* chunk_x; int* ctl; int nmax; const int64_t* cp; };
-  Tier tiers[2];
-  const int workers[2] = {blocks * kWarps, big_blocks};
-  const int64_t* cps[2] = {ps - x0, pb - x0};
-  for (int k = 0; k < 2; ++k) {
-    Tier& T = tiers[k];
-    T.workers = workers[k];
-    T.nmax = 10 * T.workers + 8;
-    T.chunk_r = sc.alloc<int64_t>(T.nmax + 1);
-    T.chunk_x = sc.alloc<int32_t>(T.nmax);
-    T.ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
-    T.cp = cps[k];
-    TC_CUDA(cudaMemsetAsync(T.ctl, 0, 2 * sizeof(int), s));
-    k_plan<<<grid_for(T.nmax + 1, 256), 256, 0, s>>>(T.cp, row_indptr, x0, x1, T.workers, T.nmax, T.chunk_r,
-                                                     T.chunk_x, T.ctl, mode);
+  size_t tmp = 0, tmp2 = 0;
+  TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag[0], flag[0], nx + 1, s));
+  TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (int64_t*)nullptr, (int64_t*)nullptr, nx + 1, s));
+  void* t = sc.bytes(std::max(tmp, tmp2));
+  EngineArgs args[3];
+  for (int k = 0; k < 3; ++k) {
+    int32_t* pos = sc.alloc<int32_t>(nx + 1);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, flag[k], pos, nx + 1, s));
+    int32_t* own = sc.alloc<int32_t>(nx + 1);
+    int64_t* len = sc.alloc<int64_t>(nx + 1);
+    int64_t* cst = sc.alloc<int64_t>(nx + 1);
+    int64_t* vrow = sc.alloc<int64_t>(nx + 1);
+    int64_t* vcost = sc.alloc<int64_t>(nx + 1);
+    TC_CUDA(cudaMemsetAsync(len, 0, (nx + 1) * sizeof(int64_t), s));
+    TC_CUDA(cudaMemsetAsync(cst, 0, (nx + 1) * sizeof(int64_t), s));
+    k_tier_scatter<<<grid, 256, 0, s>>>(flag[k], pos, x0, nx, row_indptr, cp, own, len, cst);
     check_launch();
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, len, vrow, nx + 1, s));
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, cst, vcost, nx + 1, s));
+    const int nmax = 10 * ts.workers[k] + 8;
+    int64_t* chunk_r = sc.alloc<int64_t>(nmax + 1);
+    int32_t* chunk_x = sc.alloc<int32_t>(nmax);
+    int* ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
+    TC_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
+    k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(vcost, vrow, 0, nx, ts.workers[k], nmax, chunk_r, chunk_x, ctl,
+                                                   mode);
+    check_launch();
+    const int64_t lo = k == 0 ? 0 : (k == 1 ? c0 : c1);
+    const int64_t hi = k == 0 ? c0 : (k == 1 ? c1 : INT64_MAX);
+    args[k] = EngineArgs{vrow, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
+                         bucket_bounds, nbuckets, out, nx, owner_map, lo, hi, g_big_cap, own, row_indptr};
   }
   if (g_time_engine) {
     if (!g_ev[0]) {
@@ -664,21 +772,29 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
       TC_CUDA(cudaEventCreate(&g_ev[1]));
     }
     TC_CUDA(cudaEventRecord(g_ev[0], s));
+    if (!g_tev[0])
+      for (auto& e : g_tev) TC_CUDA(cudaEventCreate(&e));
+    TC_CUDA(cudaEventRecord(g_tev[0], s));
   }
-  EngineArgs a0{row_indptr, tab_indptr, tab_indices, pool, tiers[0].chunk_r, tiers[0].chunk_x, tiers[0].ctl,
-                tiers[0].ctl + 1, bucket_bounds, nbuckets, out, n_owner, owner_map, g_warp_cap, g_big_cap};
-  k_engine<Segs><<<blocks, kThreads, 0, s>>>(a0, segs);
+  K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(args[0], segs);
   check_launch();
-  EngineArgs a1{row_indptr, tab_indptr, tab_indices, pool, tiers[1].chunk_r, tiers[1].chunk_x, tiers[1].ctl,
-                tiers[1].ctl + 1, bucket_bounds, nbuckets, out, n_owner, owner_map, g_warp_cap, g_big_cap};
-  k_engine_big<Segs><<<big_blocks, kBigThreads, kBigSmem, s>>>(a1, segs);
+  if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[1], s));
+  K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(args[1], segs);
+  check_launch();
+  if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[2], s));
+  k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(args[2], segs);
   check_launch();
   if (g_time_engine) {
+    TC_CUDA(cudaEventRecord(g_tev[3], s));
     TC_CUDA(cudaEventRecord(g_ev[1], s));
     TC_CUDA(cudaEventSynchronize(g_ev[1]));
     float ms = 0.f;
     TC_CUDA(cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]));
     g_engine_ms += ms;
+    for (int k = 0; k < 3; ++k) {
+      TC_CUDA(cudaEventElapsedTime(&ms, g_tev[k], g_tev[k + 1]));
+      g_tier_ms[k] += ms;
+    }
     ++g_engine_launches;
   }
 }
@@ -812,14 +928,17 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
   });
 }
 
-int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host) {
+int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host, double* tier_ms_host) {
   return tcb::guarded([&] {
     if (total_ms_host) *total_ms_host = tcb::g_engine_ms;
     if (launches_host) *launches_host = tcb::g_engine_launches;
+    if (tier_ms_host)
+      for (int k = 0; k < 3; ++k) tier_ms_host[k] = tcb::g_tier_ms[k];
     if (enable >= 0) {
       tcb::g_time_engine = enable != 0;
       tcb::g_engine_ms = 0.0;
       tcb::g_engine_launches = 0;
+      for (int k = 0; k < 3; ++k) tcb::g_tier_ms[k] = 0.0;
     }
   });
 }
@@ -829,6 +948,9 @@ int tc_set_tuning(int32_t key, int64_t value) {
     if (key == 0) {
       TC_REQUIRE(value >= 0 && value <= tcb::kTabCap, TC_EINVAL, "warp cap out of range");
       tcb::g_warp_cap = (int)value;
+    } else if (key == 2) {
+      TC_REQUIRE(value >= 0 && value <= tcb::kMidCap, TC_EINVAL, "mid cap out of range");
+      tcb::g_mid_cap = (int)value;
     } else if (key == 1) {
       TC_REQUIRE(value >= 0 && value <= tcb::kBigCap, TC_EINVAL, "block cap out of range");
       tcb::g_big_cap = (int)value;

@@ -300,16 +300,18 @@ def test_rmat_scale_properties():
     assert int(g.deg.sum()) == 2 * g.m
 
 
-@pytest.mark.parametrize("caps", [(0, 4096), (8, 4096), (8, 8), (0, 0)])
+@pytest.mark.parametrize("caps", [(0, 1024, 4096), (8, 16, 4096), (8, 16, 8), (0, 0, 0)])
 def test_engine_tiers_forced(caps):
-    """Force owners through the block tier (warp cap lowered) and through
-    the global-memory fallback (block cap lowered); results must not move."""
+    """Force owners through the mid warp tier, the block tier (warp caps
+    lowered) and the global-memory fallback (block cap lowered); results
+    must not move.  caps = (small cap, mid cap, block cap)."""
     from paper_1406_5687_b200 import _lib
     L = _lib.lib()
     cases = ["pa_2000_10_3", "rmat_s10", "sparse_labels", "er_150_0.5_5", "gnm_2000_16000"]
     try:
         _lib.check(L.tc_set_tuning(0, caps[0]))
-        _lib.check(L.tc_set_tuning(1, caps[1]))
+        _lib.check(L.tc_set_tuning(2, caps[1]))
+        _lib.check(L.tc_set_tuning(1, caps[2]))
         for name in cases:
             case = SMALL[name]
             _, g = graph_of(name)
@@ -322,6 +324,7 @@ def test_engine_tiers_forced(caps):
             assert host(count_lowest(g, 0, g.n, bounds=b)).tolist() == case["lowest_5"].tolist(), name
     finally:
         L.tc_set_tuning(0, 256)
+        L.tc_set_tuning(2, 1024)
         L.tc_set_tuning(1, 4096)
 
 

@@ -42,15 +42,16 @@ for cfg in a.configs.split(","):
     print(f"{cfg}: tiles={ti.ntiles} virtual owners={ti.k}", flush=True)
     for name, fn in engines:
         T = int(fn().item())
-        _lib.lib().tc_engine_timing(1, None, None)
+        _lib.lib().tc_engine_timing(1, None, None, None)
         for _ in range(a.reps):
             flush.fill_(1)
             fn()
         torch.cuda.synchronize()
         tot, nl = ctypes.c_double(), ctypes.c_longlong()
-        _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl))
+        tiers = (ctypes.c_double * 3)()
+        _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl), tiers)
         ms = tot.value / nl.value
         print(f"{cfg} {name}: n={g.n} m={g.m} T={T} engine {ms:.3f} ms  -> {g.m / ms / 1e6:.2f} G edges/s; "
-              f"build {build_ms:.1f} ms; gen {tg:.1f}s", flush=True)
+              f"build {build_ms:.1f} ms; gen {tg:.1f}s; tiers ms " + " / ".join(f"{x / nl.value:.2f}" for x in tiers), flush=True)
     del g, dev_raw
     torch.cuda.empty_cache()
