@@ -142,7 +142,7 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
 int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host, double* tier_ms_host);
 
 /* Engine tier caps (testing / tuning): key 0 = small warp-tier table cap
- * (0..256, default 256), key 2 = mid warp-tier cap (0..1024, default 1024),
+ * (0..256, default 256), key 2 = mid warp-tier cap (0..512, default 512),
  * key 1 = block-tier staged-table cap (0..4096, default 4096; larger tables
  * use binary search in global memory). */
 int tc_set_tuning(int32_t key, int64_t value);

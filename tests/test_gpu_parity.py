@@ -300,7 +300,7 @@ def test_rmat_scale_properties():
     assert int(g.deg.sum()) == 2 * g.m
 
 
-@pytest.mark.parametrize("caps", [(0, 1024, 4096), (8, 16, 4096), (8, 16, 8), (0, 0, 0)])
+@pytest.mark.parametrize("caps", [(0, 512, 4096), (8, 16, 4096), (8, 16, 8), (0, 0, 0)])
 def test_engine_tiers_forced(caps):
     """Force owners through the mid warp tier, the block tier (warp caps
     lowered) and the global-memory fallback (block cap lowered); results
@@ -324,7 +324,7 @@ def test_engine_tiers_forced(caps):
             assert host(count_lowest(g, 0, g.n, bounds=b)).tolist() == case["lowest_5"].tolist(), name
     finally:
         L.tc_set_tuning(0, 256)
-        L.tc_set_tuning(2, 1024)
+        L.tc_set_tuning(2, 512)
         L.tc_set_tuning(1, 4096)
 
 
