@@ -223,6 +223,22 @@ int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int
                     const int64_t* tab_indptr, int64_t* row_indptr, int64_t* row_segs,
                     int64_t* cost_prefix, tc_stream_t stream);
 
+/* ------------------------------------------------------------ ingestion */
+
+/* load_edge_list (graph_io.py:42-71) on the device: buf = the file's bytes
+ * (device).  Lines split on '\n'; blank lines and lines whose first token
+ * starts with '#' are skipped; every other line must hold exactly two
+ * Python-int() tokens (sign, ASCII digits, single underscores between
+ * digits) with non-negative values < 2^31.  On success out_pairs int32
+ * [2*cap] (cap >= nbytes/4 + 1 always suffices) gets the pairs in file
+ * order and n = max id + 1.  On the first malformed line *err_line_host =
+ * its 1-based number, *err_code_host = 2 (token count, *err_tokens_host
+ * holds it), 3 (non-integer), 4 (negative) or 5 (exceeds int32).
+ * Synchronises. */
+int tc_parse_edge_list(const unsigned char* buf, int64_t nbytes, int32_t* out_pairs, int64_t cap,
+                       int64_t* m_host, int64_t* n_host, int64_t* err_line_host, int32_t* err_code_host,
+                       int32_t* err_tokens_host, tc_stream_t stream);
+
 /* ------------------------------------------------------------ generators */
 
 /* ER G(n,m) raw pairs (configs 1, 5): out int32[2m]. */

@@ -45,6 +45,8 @@ _SIGS = {
     "tc_surrogate_pack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_owner_segments": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _pi64, _vp],
     "tc_segments_csr": [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
+    "tc_parse_edge_list": [_vp, _i64, _vp, _i64, _pi64, _pi64, _pi64, ctypes.POINTER(ctypes.c_int32),
+                           ctypes.POINTER(ctypes.c_int32), _vp],
     "tc_gen_er": [_i64, _i64, _u64, _vp, _vp],
     "tc_gen_rmat": [_i32, _i64, _u64, _vp, _vp],
     "tc_gen_chung_lu": [_i64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _u64, _vp, _i64, _pi64, _vp],

@@ -125,6 +125,49 @@ def reference_outputs(tc, raw_edges):
     return out
 
 
+PARSE_INPUTS = [
+    b"# c\n0 1\n\n1 2\n", b"0 1\n0 1\n", b"0 x\n", b"0 1\n1 2 3\n", b"0 -1\n", b"1_000 2\n",
+    b"  7\t8  \r\n# x\n\n9 10", b"+3 -0\n", b"1__0 2\n", b"a b c\n0 1\n", b"\x1c1\x1d2\x1e\n",
+    b"0 1\n#\n   \n2 3 # c\n", b"0 1\n\xff 2\n", b"x -1\n", b"-1 x\n", b"3 4\n-2 5\n", b"\n\n", b"5 5\n5 5",
+    b"007 08\n", b"1 2\x0b\x0c\n3\t\t4\n", b"12 2147483647\n",
+]
+
+
+def parse_cases(tc):
+    """The reference's load_edge_list on edge cases and on a larger random
+    file: expected edges, or (lineno, message) of the EdgeListParseError."""
+    cases = list(PARSE_INPUTS)
+    rng = np.random.default_rng(11)
+    lines = []
+    for i in range(3000):
+        r = rng.random()
+        if r < 0.05:
+            lines.append(b"# comment %d" % i)
+        elif r < 0.08:
+            lines.append(b"   ")
+        else:
+            u, v = rng.integers(0, 10**6, size=2)
+            sep = [b" ", b"\t", b"  "][i % 3]
+            lines.append(b"%d%s%d" % (u, sep, v))
+    cases.append(b"\n".join(lines) + b"\n")
+    out = []
+    for data in cases:
+        rec = {"input": data.decode("latin-1")}
+        try:
+            raw = tc.load_edge_list(data)
+            rec["n"] = int(raw.n)
+            if len(raw.edges) > 50:
+                rec["m"] = int(len(raw.edges))
+                rec["edges_checksum"] = gen_twin.checksum(raw.edges)
+            else:
+                rec["edges"] = raw.edges.tolist()
+        except tc.EdgeListParseError as e:
+            rec["lineno"] = e.lineno
+            rec["message"] = str(e)
+        out.append(rec)
+    return out
+
+
 def known_answers(tc):
     def gp(pairs, n=None):
         return tc.build_graph(tc.normalize(tc.RawGraph.from_pairs(pairs, n=n)))
@@ -166,6 +209,7 @@ def known_answers(tc):
         tc.dedup_send_targets(np.array([3, 4, 9]), np.array([0, 5, 10])),
         tc.dedup_send_targets(np.array([3, 4, 9]), np.array([0, 5, 10]), self_rank=0),
     ]
+    k["parse"] = parse_cases(tc)
     k["surrogate_count_k3"] = [
         tc.surrogate_count([], tc.NodeRange(0, 3), k3),
         tc.surrogate_count(k3.succ(0), tc.NodeRange(2, 1), k3),

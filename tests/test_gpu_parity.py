@@ -426,3 +426,44 @@ def test_full_scale_configs(cfg):
     assert total == want["T"]
     del g
     torch.cuda.empty_cache()
+
+
+def test_load_edge_list_device_parser(known):
+    """Device edge-list ingestion vs the reference's load_edge_list on edge
+    cases (comments, blanks, CR/LF, unicode-space bytes, underscores, signs,
+    non-ASCII, token counts) and a 3000-line random file."""
+    for rec in known["parse"]:
+        data = rec["input"].encode("latin-1")
+        if "lineno" in rec:
+            with pytest.raises(tcb.EdgeListParseError) as e:
+                tcb.load_edge_list(data)
+            assert e.value.lineno == rec["lineno"]
+            assert str(e.value) == rec["message"]
+            continue
+        raw = tcb.load_edge_list(data)
+        got = host(raw.edges).reshape(-1, 2)
+        assert raw.n == rec["n"]
+        if "edges" in rec:
+            assert got.tolist() == rec["edges"]
+        else:
+            assert len(got) == rec["m"] and gen_twin.checksum(got) == rec["edges_checksum"]
+    g = tcb.build_graph(tcb.normalize(tcb.load_edge_list(b"# c\n0 1\n1 2\n0 2\n")))
+    assert tcb.count_triangles_seq(g) == 1
+
+
+def test_export_import_round_trip(tmp_path):
+    """export_edge_list -> load_edge_list -> normalize is a fixed point
+    (graph_io.py:79-99; the reference's round-trip tests)."""
+    import io
+    for name in ("er_40_0.3_11", "pa_500_8_11", "star"):
+        _, g = graph_of(name)
+        out = io.StringIO()
+        tcb.export_edge_list(g, out)
+        g2 = tcb.build_graph(tcb.normalize(tcb.load_edge_list(out.getvalue().encode())))
+        assert np.array_equal(host(g2.relabel), np.arange(g2.n))
+        assert np.array_equal(host(g2.eff_indptr), host(g.eff_indptr))
+        assert np.array_equal(host(g2.eff_indices), host(g.eff_indices))
+        path = tmp_path / f"{name}.txt"
+        tcb.export_edge_list(g, path)
+        g3 = tcb.build_graph(tcb.normalize(tcb.load_edge_list_path(path)))
+        assert tcb.count_triangles_seq(g3) == tcb.count_triangles_seq(g)
