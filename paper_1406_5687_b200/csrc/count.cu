@@ -654,10 +654,13 @@ static long long g_engine_launches = 0;
 
 // Engine tiers (same order as the cost split): small / mid warp tiers, block tier.
 #ifndef TCB_MID_WINDOWS
-#define TCB_MID_WINDOWS 4
+#define TCB_MID_WINDOWS 2
 #endif
 #define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin>
-#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, 1, TCB_MID_WINDOWS>
+#ifndef TCB_MID_MINB
+#define TCB_MID_MINB 6
+#endif
+#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS>
 
 struct TierShape {
   int blocks[3];   // persistent grid per tier
@@ -688,7 +691,8 @@ static const TierShape& tier_shape() {
 // Tier of each owner in [x0, x1) (flags; owners without cost join no tier).
 __global__ void k_tier_flags(const int64_t* __restrict__ cp, int64_t x0, int64_t x1,
                              const int32_t* __restrict__ owner_map, const int64_t* __restrict__ tab_indptr,
-                             int c0, int c1, int32_t* f0, int32_t* f1, int32_t* f2) {
+                             int c0, int c1, int32_t* f0, int32_t* f1, int32_t* f2, unsigned long long* sizes) {
+  unsigned long long c[3] = {0, 0, 0};
   GRID_STRIDE(i, x1 - x0 + 1) {
     int64_t x = x0 + i;
     int t = -1;
@@ -700,6 +704,12 @@ __global__ void k_tier_flags(const int64_t* __restrict__ cp, int64_t x0, int64_t
     f0[i] = t == 0;
     f1[i] = t == 1;
     f2[i] = t == 2;
+    if (t >= 0) ++c[t];
+  }
+  for (int k = 0; k < 3; ++k) {
+    unsigned long long v = c[k];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sizes[k], v);
   }
 }
 
@@ -732,14 +742,20 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
   const int grid = grid_for(nx + 1, 256, sm_count() * 16);
   int32_t* flag[3];
   for (int k = 0; k < 3; ++k) flag[k] = sc.alloc<int32_t>(nx + 1);
-  k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2]);
+  auto* sizes = sc.alloc<unsigned long long>(3);
+  TC_CUDA(cudaMemsetAsync(sizes, 0, 3 * sizeof(unsigned long long), s));
+  k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2], sizes);
   check_launch();
+  unsigned long long hsz[3];
+  TC_CUDA(cudaMemcpyAsync(hsz, sizes, sizeof(hsz), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);  // empty tiers are skipped entirely
   size_t tmp = 0, tmp2 = 0;
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag[0], flag[0], nx + 1, s));
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (int64_t*)nullptr, (int64_t*)nullptr, nx + 1, s));
   void* t = sc.bytes(std::max(tmp, tmp2));
   EngineArgs args[3];
   for (int k = 0; k < 3; ++k) {
+    if (hsz[k] == 0) continue;
     int32_t* pos = sc.alloc<int32_t>(nx + 1);
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, flag[k], pos, nx + 1, s));
     int32_t* own = sc.alloc<int32_t>(nx + 1);
@@ -776,14 +792,20 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
       for (auto& e : g_tev) TC_CUDA(cudaEventCreate(&e));
     TC_CUDA(cudaEventRecord(g_tev[0], s));
   }
-  K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(args[0], segs);
-  check_launch();
+  if (hsz[0]) {
+    K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(args[0], segs);
+    check_launch();
+  }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[1], s));
-  K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(args[1], segs);
-  check_launch();
+  if (hsz[1]) {
+    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(args[1], segs);
+    check_launch();
+  }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[2], s));
-  k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(args[2], segs);
-  check_launch();
+  if (hsz[2]) {
+    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(args[2], segs);
+    check_launch();
+  }
   if (g_time_engine) {
     TC_CUDA(cudaEventRecord(g_tev[3], s));
     TC_CUDA(cudaEventRecord(g_ev[1], s));
