@@ -12,20 +12,22 @@
 //        count_node_range(v0, v1) (_kernels.py:40-52) with per-bucket
 //        partials, used for count_task / count_dynamic.
 //
-// Two tiers by table size (the shape-bucketing of SURVEY.md §7 step 6):
-//   warp tier  (d <= 256): a warp stages the owner's list in its own
-//              shared-memory slice -- sorted copy + 16K-bit hashed filter.
-//   block tier (d  > 256): a 512-thread block stages up to 16K entries plus
-//              a 1M-bit filter (192 KB) and all 16 warps stream the owner's
-//              segments -- the skewed pairs of Chung-Lu / R-MAT hubs.
-//              Beyond 16K entries the probes fall back to binary search in
-//              global memory (L1/L2 resident).
-// Segment streaming (both tiers): a warp takes 32 segments, compacts the
+// Three tiers by table size d (the shape bucketing of SURVEY.md §7 step 6);
+// each tier runs over a compacted list of its own owners:
+//   small  (d <= 256): a warp owns a 4 KB shared slice -- 16K-bit hashed
+//          filter + bucketized hash table (2^7 buckets of 4 ids);
+//   mid    (d <= 512): the same with 8 KB slices (4 warps per block);
+//   block  (d  > 512): a 512-thread block stages up to 4096 ids (256K-bit
+//          filter + 2^11 buckets) and all 16 warps stream the owner's
+//          segments -- the hubs of Chung-Lu / R-MAT; beyond 4096 ids the
+//          probes use binary search in global memory (L1/L2 resident).
+// Segment streaming (all tiers): a warp takes 32 segments, compacts the
 // non-empty ones, and flattens the 16-byte chunks they touch with a warp
 // scan; lane j of a window loads chunk base+j as one int4 (4 list ids),
-// resolving its segment with one ballot + one redux.or + popc.  A probe is a
-// range check, one filter LDS and three ALU ops, branch-free over the 4 ids;
-// only filter hits take the binary-search verification in the sorted copy.
+// resolving its segment with one ballot + one redux.or + popc.  A probe is
+// one filter LDS and three ALU ops, branch-free over the 4 ids; only filter
+// hits are verified (one LDS.128 in the bucket table: inline in the warp
+// tiers, queued and verified in bulk in the block tier).
 //
 // Load balance (the paper's dynamic load balancing, PAPER.md:788-822,
 // dynamic_lb.py:68-109, restated for warps): each tier splits its owners'
@@ -176,15 +178,6 @@ __device__ __forceinline__ bool bkt_lookup(const int4* bkt, int lb, int32_t x) {
   }
 }
 
-__device__ __forceinline__ bool bsearch_smem(const int32_t* t, int d, int32_t w) {
-  int lo = 0, hi = d;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (t[mid] < w) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo < d && t[lo] == w;
-}
 
 __device__ __forceinline__ bool bsearch_gmem(const int32_t* __restrict__ t, int64_t d, int32_t w) {
   int64_t lo = 0, hi = d;
