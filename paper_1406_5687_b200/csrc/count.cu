@@ -71,7 +71,7 @@ static constexpr int kTabCost = 16;
 static constexpr int32_t kEmpty = -1;
 
 // Verification kinds of a staged table (see probe4).
-enum : int { kGlobal = 0, kInline = 1, kBuckets = 2 };
+enum : int { kGlobal = 0, kInline = 1, kBuckets = 2, kExact = 3 };
 
 template <int kLb, int kLw>
 struct WarpSliceT {
@@ -198,6 +198,7 @@ struct Table {
   int lb;
   int32_t tmin, tmax;
   int dmax;             // max bucket displacement (kInline)
+  uint32_t span;        // kExact: bit (id - tmin) of bm, ids in [tmin, tmin + span)
 };
 
 // Verify the queued filter hits of this warp (kBuckets) and empty the queue.
@@ -218,6 +219,17 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (((vmask >> k) & 1u) && xs[k] >= t.tmin && xs[k] <= t.tmax) cnt += bsearch_gmem(t.tab, t.d, xs[k]);
+    return;
+  }
+  if (kKind == kExact) {  // direct-mapped exact bitmap: no hashing, no verification
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t off = (uint32_t)(xs[k] - t.tmin);
+      const uint32_t wd = off < t.span ? t.bm[off >> 5] : 0u;
+      m |= ((wd >> (off & 31)) & 1u) << k;
+    }
+    cnt += __popc(m & vmask);
     return;
   }
   uint32_t m = 0;
@@ -450,6 +462,26 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       if (d <= a.d_lo || d > a.d_hi) continue;
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + t0;
+      const int32_t tlo = __ldg(&gtab[0]);
+      const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
+      if (span <= (32u << kLw)) {
+        // Narrow id span (hub owners at the top of the degree order): the
+        // filter words become an exact direct-mapped bitmap over [tlo, tlo+span).
+        for (int i = lane; i < d; i += 32) {
+          const uint32_t off = (uint32_t)(__ldg(&gtab[i]) - tlo);
+          atomicOr(&sl.bm[off >> 5], 1u << (off & 31));
+        }
+        __syncwarp();
+        Table t{sl.bm, nullptr, nullptr, nullptr, d, 0, tlo, 0, 0, span};
+        int npos = 0;
+        for (int64_t g = ra; g < rb; g += 32)
+          stream_group<kExact, kLw, Segs, kTabCap, kW>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
+                                                       lane, npos, acc.cnt);
+        __syncwarp();
+        for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
+        __syncwarp();
+        continue;
+      }
       const int lb = min(tab_lb(d), kLb);
       for (int i = lane; i < (1 << lb); i += 32) sl.bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
       __syncwarp();
@@ -460,7 +492,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         disp = max(disp, bkt_insert(sl.bkt, lb, w));
       }
       disp = __reduce_max_sync(FULL, disp);
-      Table t{sl.bm, nullptr, sl.bkt, nullptr, d, lb, 0, 0, disp};
+      Table t{sl.bm, nullptr, sl.bkt, nullptr, d, lb, 0, 0, disp, 0};
       __syncwarp();
       int npos = 0;
       for (int64_t g = ra; g < rb; g += 32)
@@ -485,6 +517,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
   int32_t* pos = reinterpret_cast<int32_t*>(big_smem + (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig)) +
                  (threadIdx.x >> 5) * kPosCap;
   __shared__ int s_chunk;
+  __shared__ int s_next;  // next segment group of the current staged owner (dynamic claiming)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kBigWarps;
   const int nch = *a.nchunks;
   for (int i = threadIdx.x; i < (1 << kLwBig); i += kBigThreads) bm[i] = 0;
@@ -492,10 +525,16 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
   int64_t staged = -1;  // node whose table is staged
   const int32_t* staged_list = nullptr;
   int64_t staged_d = 0;
+  bool staged_exact = false;
+  int32_t staged_lo = 0;
+  uint32_t staged_span = 0;
 
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_chunk = atomicAdd(a.queue, 1);
+    if (threadIdx.x == 0) {
+      s_chunk = atomicAdd(a.queue, 1);
+      s_next = 0;
+    }
     __syncthreads();
     const int c = s_chunk;
     if (c >= nch) break;
@@ -519,27 +558,58 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
       if (d <= a.big_cap) {
         if (staged != u) {
           __syncthreads();
-          for (int i = threadIdx.x; i < staged_d; i += kBigThreads) filt_clear<kLwBig>(bm, __ldg(&staged_list[i]));
-          for (int i = threadIdx.x; i < (1 << lb); i += kBigThreads) bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
+          if (threadIdx.x == 0) s_next = 0;
+          if (staged_exact) {
+            for (int i = threadIdx.x; i < staged_d; i += kBigThreads)
+              bm[(uint32_t)(__ldg(&staged_list[i]) - staged_lo) >> 5] = 0;
+          } else {
+            for (int i = threadIdx.x; i < staged_d; i += kBigThreads) filt_clear<kLwBig>(bm, __ldg(&staged_list[i]));
+          }
+          const int32_t tlo = __ldg(&gtab[0]);
+          const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
+          const bool exact = span <= (32u << kLwBig);
+          if (!exact)
+            for (int i = threadIdx.x; i < (1 << lb); i += kBigThreads) bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncthreads();
           for (int i = threadIdx.x; i < d; i += kBigThreads) {
             const int32_t w = __ldg(&gtab[i]);
-            filt_insert<kLwBig>(bm, w);
-            bkt_insert(bkt, lb, w);
+            if (exact) {
+              const uint32_t off = (uint32_t)(w - tlo);
+              atomicOr(&bm[off >> 5], 1u << (off & 31));
+            } else {
+              filt_insert<kLwBig>(bm, w);
+              bkt_insert(bkt, lb, w);
+            }
           }
           __syncthreads();
           staged = u;
           staged_list = gtab;
           staged_d = d;
+          staged_exact = exact;
+          staged_lo = tlo;
+          staged_span = span;
         }
-        Table t{bm, nullptr, bkt, pos, d, lb, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
+        Table t{bm, nullptr, bkt, pos, d, lb, staged_lo, 0, 0, staged_span};
         int npos = 0;
-        for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kBuckets, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+        // Groups are claimed dynamically: every owner change passes a block
+        // barrier (restage or chunk fetch) that reset s_next, and the wait at
+        // the next barrier is at most one group long.
+        for (;;) {
+          int gi = 0;
+          if (lane == 0) gi = atomicAdd(&s_next, 1);
+          gi = __shfl_sync(0xffffffffu, gi, 0);
+          const int64_t g = ra + 32 * (int64_t)gi;
+          if (g >= rb) break;
+          if (staged_exact)
+            stream_group<kExact, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
                                          acc.cnt);
-        drain(t, npos, lane, acc.cnt);
+          else
+            stream_group<kBuckets, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+                                           acc.cnt);
+        }
+        if (!staged_exact) drain(t, npos, lane, acc.cnt);
       } else {
-        Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1])};
+        Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1]), 0, 0};
         int npos = 0;
         for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
           stream_group<kGlobal, 0>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
@@ -675,10 +745,85 @@ static const TierShape& tier_shape() {
     TC_CUDA(cudaFuncSetAttribute(k_engine_big<PushSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine_big<PullSegs>, kBigThreads, kBigSmem));
     ts.blocks[2] = std::max(per_sm, 1) * sm_count();
-    ts.workers[2] = ts.blocks[2];
+#ifndef TCB_BIG_WORKERS_X4
+#define TCB_BIG_WORKERS_X4 4
+#endif
+    ts.workers[2] = std::max(1, ts.blocks[2] * TCB_BIG_WORKERS_X4 / 4);
     init = true;
   }
   return ts;
+}
+
+// Exact per-segment cost of a tier (warp per tier owner): segment length +
+// kSegCost, plus the owner's table build (d + kTabCost) on its first segment.
+template <class Segs>
+__global__ void k_seg_cost(const int32_t* __restrict__ own, const int64_t* __restrict__ vrow,
+                           const int64_t* __restrict__ phys_row, const int32_t* __restrict__ owner_map,
+                           const int64_t* __restrict__ tab_indptr, int64_t k, Segs segs, int64_t* cost) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = warp; x < k; x += nwarps) {
+    const int64_t o = own[x];
+    const int64_t u = owner_map ? (int64_t)owner_map[o] : o;
+    const int64_t d = tab_indptr[u + 1] - tab_indptr[u];
+    const int64_t r0 = vrow[x], r1 = vrow[x + 1], p0 = phys_row[o];
+    for (int64_t r = r0 + lane; r < r1; r += 32) {
+      int64_t s = 0, e = 0;
+      segs.get(p0 + (r - r0), s, e);
+      cost[r] = (e - s) + kSegCost + (r == r0 ? d + kTabCost : 0);
+    }
+  }
+}
+
+// Chunk boundaries from an exact per-segment cost prefix (sp, nseg + 1):
+// the same schedule as k_plan, but a threshold maps to a segment index by
+// binary search instead of a proportional split inside the owner.
+__global__ void k_plan_seg(const int64_t* __restrict__ sp, int64_t nseg, const int64_t* __restrict__ vrow,
+                           int64_t nx, int nW, int nmax, int64_t* chunk_r, int32_t* chunk_x, int* nchunks) {
+  const int64_t C = sp[nseg];
+  const double Cd = (double)C;
+  const int nfirst = 6 * nW;
+  const double half = floor(Cd * 0.75);
+  const double R0 = Cd - half;
+  const double q = 1.0 - 1.0 / (double)nW;
+  const double minc = fmax(Cd / (32.0 * nW), 64.0);
+  int64_t J = 0;
+  if (nW > 1 && R0 / nW > minc) J = (int64_t)ceil(log(minc * nW / R0) / log(q));
+  if (J < 0) J = 0;
+  const double RJ = R0 * pow(q, (double)J);
+  const int64_t ntail = (int64_t)ceil(RJ / minc);
+  int64_t total = (C == 0) ? 0 : (int64_t)nfirst + J + ntail;
+  if (total > nmax) total = nmax;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nchunks = (int)total;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nmax; i += (int64_t)gridDim.x * blockDim.x) {
+    double t;
+    if (i >= total) t = Cd;
+    else if (i <= nfirst) t = floor((double)i * half / (double)nfirst);
+    else {
+      int64_t j = i - nfirst;
+      if (j <= J) t = half + R0 * (1.0 - pow(q, (double)j));
+      else t = half + (R0 - RJ) + (double)(j - J) * minc;
+    }
+    int64_t T = (int64_t)t;
+    if (T > C) T = C;
+    if (T < 0) T = 0;
+    int64_t lo = 0, hi = nseg;  // first segment r with sp[r] >= T
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sp[mid] < T) lo = mid + 1;
+      else hi = mid;
+    }
+    const int64_t r = (T >= C) ? nseg : lo;
+    int64_t a = 0, b = nx;  // owner: largest x with vrow[x] <= r
+    while (b - a > 1) {
+      int64_t mid = (a + b) >> 1;
+      if (vrow[mid] <= r) a = mid;
+      else b = mid;
+    }
+    chunk_r[i] = r;
+    if (i < nmax) chunk_x[i] = (int32_t)a;
+  }
 }
 
 // Tier of each owner in [x0, x1) (flags; owners without cost join no tier).
@@ -767,8 +912,26 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
     int32_t* chunk_x = sc.alloc<int32_t>(nmax);
     int* ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
     TC_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
-    k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(vcost, vrow, 0, nx, ts.workers[k], nmax, chunk_r, chunk_x, ctl,
-                                                   mode);
+    if (k == 2) {  // block tier: hub segments vary wildly in cost -> plan on an exact per-segment prefix
+      int64_t nseg = 0;
+      TC_CUDA(cudaMemcpyAsync(&nseg, vrow + nx, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      sync_stream(s);
+      int64_t* scost = sc.alloc<int64_t>(nseg + 1);
+      int64_t* sp = sc.alloc<int64_t>(nseg + 1);
+      TC_CUDA(cudaMemsetAsync(scost + nseg, 0, sizeof(int64_t), s));
+      k_seg_cost<<<grid_for((int64_t)hsz[k] * 32, 256, sm_count() * 16), 256, 0, s>>>(
+          own, vrow, row_indptr, owner_map, tab_indptr, (int64_t)hsz[k], segs, scost);
+      check_launch();
+      size_t tmp3 = 0;
+      TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp3, scost, sp, nseg + 1, s));
+      void* t3 = sc.bytes(tmp3);
+      TC_CUDA(cub::DeviceScan::ExclusiveSum(t3, tmp3, scost, sp, nseg + 1, s));
+      k_plan_seg<<<grid_for(nmax + 1, 256), 256, 0, s>>>(sp, nseg, vrow, nx, ts.workers[k], nmax, chunk_r, chunk_x,
+                                                         ctl);
+    } else {
+      k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(vcost, vrow, 0, nx, ts.workers[k], nmax, chunk_r, chunk_x, ctl,
+                                                     mode);
+    }
     check_launch();
     const int64_t lo = k == 0 ? 0 : (k == 1 ? c0 : c1);
     const int64_t hi = k == 0 ? c0 : (k == 1 ? c1 : INT64_MAX);

@@ -1,0 +1,40 @@
+"""Small workload for compute-sanitizer: every engine tier (forced caps), both
+formulations, partitioning, surrogate, parser, generators (dev/CI tool)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import torch  # noqa: E402
+
+import paper_1406_5687_b200 as tcb  # noqa: E402
+from paper_1406_5687_b200 import _lib  # noqa: E402
+from paper_1406_5687_b200.distributed import emulate_ranks  # noqa: E402
+from paper_1406_5687_b200.graph_io import er_edges, rmat_edges  # noqa: E402
+from paper_1406_5687_b200.sequential import count_lowest  # noqa: E402
+
+L = _lib.lib()
+graphs = []
+for raw in (er_edges(3000, 40000, 1), rmat_edges(11, 8, 2)):
+    graphs.append(tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw))))
+core = [(a, b) for a in range(300) for b in range(a + 1, 300)]
+graphs.append(tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(core))))
+for caps in ((256, 512, 4096), (0, 512, 4096), (8, 16, 4096), (8, 16, 8)):
+    _lib.check(L.tc_set_tuning(0, caps[0]))
+    _lib.check(L.tc_set_tuning(2, caps[1]))
+    _lib.check(L.tc_set_tuning(1, caps[2]))
+    for g in graphs:
+        T = tcb.count_triangles_seq(g)
+        assert int(count_lowest(g).item()) == T
+        total, _ = tcb.count_space_surrogate(g, 3)
+        assert total == T
+_lib.check(L.tc_set_tuning(0, 256))
+_lib.check(L.tc_set_tuning(2, 512))
+_lib.check(L.tc_set_tuning(1, 4096))
+for g in graphs:
+    total, _ = emulate_ranks(g, 4)
+    tcb.count_dynamic(g, 5)
+    _ = g.full_indices
+tcb.load_edge_list(b"# x\n0 1\n1 2\n2 0\n")
+torch.cuda.synchronize()
+print("sanitize workload ok")
