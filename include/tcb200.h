@@ -223,6 +223,36 @@ int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int
                     const int64_t* tab_indptr, int64_t* row_indptr, int64_t* row_segs,
                     int64_t* cost_prefix, tc_stream_t stream);
 
+/* ------------------------------------------------------------ direct scheme */
+
+/* Direct-scheme census (the per-pair counters of _direct_rank,
+ * space_efficient.py:188-231 with runtime.py:139-149 accounting) for all
+ * ranks: requests int64[P*P], requests[i*P+j] = number of oriented edges
+ * (v, u) with owner(v) = i != owner(u) = j (one TASK_REQUEST each);
+ * reply_words int64[P], reply_words[j] = sum over those pairs of
+ * (2 + d^_u) (the DATA replies j serves, runtime.py:80-81). */
+int tc_direct_census(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n, const int64_t* bounds,
+                     int32_t P, long long* requests, long long* reply_words, tc_stream_t stream);
+
+/* One rank of the deduplicated pull: the distinct ids >= hi named by the
+ * shard's lists (shard_indptr int64[nloc+1] local offsets, shard_indices
+ * global ids), ascending -- hence grouped by owner -- into req_ids
+ * int32[cap], their multiplicities (the reference's per-pair request
+ * count) into req_mult int64[cap]; counts int64[P] = distinct ids per owner,
+ * ref_counts int64[P] = requests per owner as the reference counts them.
+ * cap >= shard_indptr[nloc] always suffices.  Synchronises. */
+int tc_direct_requests(const int64_t* shard_indptr, const int32_t* shard_indices, int64_t nloc, int64_t hi,
+                       const int64_t* bounds, int32_t P, int32_t* req_ids, int64_t* req_mult, int64_t cap,
+                       long long* counts, long long* ref_counts, int64_t* nreq_host, tc_stream_t stream);
+
+/* Lookup CSR of one rank over ids [0, n_rows): row lo+i = the shard's row
+ * i, row req_ids[k] has length req_lens[k] (the fetched lists, ascending
+ * ids all >= lo + nloc), every other row empty.  out_indptr int64[n_rows+1];
+ * the matching indices are the shard's ids followed by the fetched ids. */
+int tc_direct_table(const int64_t* shard_indptr, int64_t nloc, int64_t lo, const int32_t* req_ids,
+                    const int64_t* req_lens, int64_t nreq, int64_t n_rows, int64_t* out_indptr,
+                    tc_stream_t stream);
+
 /* ------------------------------------------------------------ ingestion */
 
 /* load_edge_list (graph_io.py:42-71) on the device: buf = the file's bytes

@@ -406,6 +406,34 @@ int or_surrogate(const int64_t *indptr, const int64_t *indices, int64_t n,
     return 0;
 }
 
+/* Direct scheme (space_efficient.py:188-231): rank r counts
+ * count_node_range(lo, hi) itself (count_local_pairs + intersect_size with
+ * each fetched N^_u); one TASK_REQUEST per cross pair (v, u) to owner(u)
+ * (207-209), answered by one data_msg of 2 + d^_u words (runtime.py:80-81,
+ * space_efficient.py:195-197). */
+int or_direct(const int64_t *indptr, const int64_t *indices, int64_t n, const int64_t *bounds,
+              int64_t P, int64_t *partials, int64_t *requests, int64_t *reply_words) {
+    (void)n;
+    for (int64_t i = 0; i < P; ++i) partials[i] = reply_words[i] = 0;
+    for (int64_t i = 0; i < P * P; ++i) requests[i] = 0;
+    for (int64_t r = 0; r < P; ++r) {
+        int64_t lo = bounds[r], hi = bounds[r + 1];
+        for (int64_t v = lo; v < hi; ++v) {
+            int64_t s0 = indptr[v], s1 = indptr[v + 1], seg = r;
+            for (int64_t k = s0; k < s1; ++k) {
+                int64_t u = indices[k];
+                partials[r] += merge_count(indices, s0, s1, indices, indptr[u], indptr[u + 1]);
+                if (u >= hi) {
+                    while (bounds[seg + 1] <= u) ++seg;
+                    requests[r * P + seg]++;
+                    reply_words[seg] += 2 + (indptr[u + 1] - indptr[u]);
+                }
+            }
+        }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------ */
 /* pa_edge_list: _kernels.py:129-178 (splitmix64, resample duplicates) */
 /* ------------------------------------------------------------------ */

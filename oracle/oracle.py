@@ -48,6 +48,7 @@ def lib():
         L.or_plan_tasks.argtypes = [p, i64, i64, p, p, p, p,
                                     ctypes.POINTER(ctypes.c_double), p, p]
         L.or_surrogate.argtypes = [p, p, i64, p, i64, p, p]
+        L.or_direct.argtypes = [p, p, i64, p, i64, p, p, p]
         L.or_surrogate_count_list.argtypes = [p, p, i64, i64, p, i64]
         L.or_surrogate_count_list.restype = i64
         L.or_pa_num_edges.argtypes = [i64, i64]
@@ -200,6 +201,19 @@ def surrogate(g: OGraph, bounds):
     lib().or_surrogate(_ptr(_i64(g.eff_indptr)), _ptr(_i64(g.eff_indices)), g.n, _ptr(b), P,
                        _ptr(partials), _ptr(census))
     return partials, census.reshape(P, P)
+
+
+def direct(g: OGraph, bounds):
+    """Per-rank partials (lowest vertex), per-pair request matrix and reply
+    words of count_space_direct (space_efficient.py:188-231)."""
+    P = len(bounds) - 1
+    b = _i64(bounds)
+    partials = np.zeros(P, np.int64)
+    req = np.zeros(P * P, np.int64)
+    words = np.zeros(P, np.int64)
+    lib().or_direct(_ptr(_i64(g.eff_indptr)), _ptr(_i64(g.eff_indices)), g.n, _ptr(b), P, _ptr(partials),
+                    _ptr(req), _ptr(words))
+    return partials, req.reshape(P, P), words
 
 
 def surrogate_count_list(g: OGraph, lo, hi, x):

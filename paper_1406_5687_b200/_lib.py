@@ -40,6 +40,9 @@ _SIGS = {
     "tc_balanced_bounds": [_vp, _i64, _i64, _i64, _vp, _vp],
     "tc_plan_tasks": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _pi64, _vp],
     "tc_surrogate_census": [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
+    "tc_direct_census": [_vp, _vp, _i64, _vp, _i32, _vp, _vp, _vp],
+    "tc_direct_requests": [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "tc_direct_table": [_vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp],
     "tc_surrogate_records": [_vp, _vp, _i64, _vp, _i32, _i32, _i64, _vp, _vp, _i64, _vp, _pi64, _vp],
     "tc_surrogate_pack_sizes": [_vp, _vp, _i64, _vp, _pi64, _vp],
     "tc_surrogate_pack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp],

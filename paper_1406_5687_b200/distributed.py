@@ -1,6 +1,8 @@
 """One rank per GPU: the paper's space-efficient non-overlapping partition
-with the surrogate exchange (space_efficient.py:81-176),
-over torch.distributed (NCCL between B200s; gloo in the CPU tests).
+with the surrogate exchange (space_efficient.py:81-176)
+and the direct scheme as a deduplicated pull (space_efficient.py:179-262;
+`direct_rank` below), over torch.distributed (NCCL between B200s; gloo in
+the CPU tests).
 
 Rank r owns the consecutive canonical range V_r = [b_r, b_{r+1}) balanced by
 PRED_SUM (partitioning.py:139-141) and keeps ONLY the forward lists N^_v of
@@ -134,6 +136,45 @@ class DeviceOps:
         seg = torch.cat(segs).contiguous()
         return int(count_segments(shard.indptr, shard.indices, pool, owner, seg, int(owner.numel()), nloc))
 
+    def requests(self, shard: Shard, bounds, P, rank):
+        """Direct scheme, step 1: (req_ids int32 ascending, req_mult int64,
+        counts[P] distinct ids per owner, ref_counts[P] per-pair requests)."""
+        L = self._lib
+        dev = shard.indptr.device
+        nloc = shard.hi - shard.lo
+        b = torch.as_tensor(np.asarray(bounds, np.int64)).to(dev)
+        cap = max(1, shard.m)
+        ids = torch.empty(cap, dtype=torch.int32, device=dev)
+        mult = torch.empty(cap, dtype=torch.int64, device=dev)
+        counts = torch.empty(P, dtype=torch.int64, device=dev)
+        ref = torch.empty(P, dtype=torch.int64, device=dev)
+        k = ctypes.c_int64()
+        L.call("tc_direct_requests", L.ptr(shard.indptr), L.ptr(shard.indices), nloc, shard.hi, L.ptr(b), P,
+               L.ptr(ids), L.ptr(mult), cap, L.ptr(counts), L.ptr(ref), ctypes.byref(k), L.stream())
+        return ids[: k.value], mult[: k.value], counts.cpu().numpy(), ref.cpu().numpy()
+
+    def count_direct(self, shard: Shard, req_ids, fetched_len, fetched_ids):
+        """Direct scheme, step 4: count_node_range(lo, hi) over the shard's
+        lists and the fetched N^_u (lowest-vertex attribution)."""
+        L = self._lib
+        dev = shard.indptr.device
+        nloc = shard.hi - shard.lo
+        if nloc == 0:
+            return 0
+        nreq = int(req_ids.numel())
+        n_rows = max(shard.hi, int(req_ids[-1].item()) + 1 if nreq else 0)
+        indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+        flen = fetched_len.to(dev, torch.int64).contiguous()
+        L.call("tc_direct_table", L.ptr(shard.indptr), nloc, shard.lo, L.ptr(req_ids) if nreq else None,
+               L.ptr(flen) if nreq else None, nreq, n_rows, L.ptr(indptr), L.stream())
+        ml, mr = shard.m, int(fetched_ids.numel())
+        pool = torch.zeros(ml + mr + 4, dtype=torch.int32, device=dev)  # +4: 16-byte chunk reads
+        pool[:ml] = shard.indices[:ml]
+        pool[ml: ml + mr] = fetched_ids
+        out = torch.empty(1, dtype=torch.int64, device=dev)
+        L.call("tc_count_lowest", L.ptr(indptr), L.ptr(pool), n_rows, shard.lo, shard.hi, None, 1, L.ptr(out),
+               L.stream())
+        return int(out.item())
 
 def _a2a_counts(counts_np, group, device):
     """all_to_all of one int64 per peer (step 2)."""
@@ -239,4 +280,137 @@ def emulate_ranks(g, P, cost=None, ops=None):
         recv_ids = torch.cat([p[1].to(dev) for p in parts]) if parts else torch.zeros(0, dtype=torch.int32, device=dev)
         mets[r].triangles = int(ops.count(sh, recv_len, recv_ids))
         total += mets[r].triangles
+    return total, mets
+
+
+def _split_sums(values_np, counts_np):
+    """Per-peer sums of a peer-grouped array."""
+    out = np.zeros(len(counts_np), np.int64)
+    start = 0
+    for j, c in enumerate(np.asarray(counts_np, np.int64).tolist()):
+        out[j] = int(np.asarray(values_np[start: start + c], np.int64).sum())
+        start += c
+    return out
+
+
+def direct_rank(shard: Shard, bounds, group=None, ops=None, device=None):
+    """The direct scheme on this rank as a deduplicated rank-level pull
+    (space_efficient.py:179-231); returns (total, RankMetrics).
+
+      1. requests  distinct remote ids named by the shard's lists, ascending
+                   (= grouped by owner), with their per-pair multiplicity
+      2. ask       all_to_all of the id counts, then of the ids and
+                   multiplicities (the reference sends one TASK_REQUEST per
+                   cross pair; here one id per distinct u and rank)
+      3. serve     pack the requested N^_w lists, all_to_all them back
+      4. count     count_node_range(lo, hi) over own + fetched lists
+      5. reduce    all_reduce(SUM)
+
+    The metrics keep the reference's per-pair accounting (requests_to,
+    data_msgs_to, bytes_sent); wire_bytes is what the collectives moved."""
+    ops = ops or DeviceOps()
+    P = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    device = device or shard.indptr.device
+    met = RankMetrics(rank=rank, nranks=P)
+    met.partition_bytes = WORD_BYTES * ((shard.hi - shard.lo) + 1 + shard.m)
+
+    req_ids, req_mult, counts, ref_counts = ops.requests(shard, bounds, P, rank)          # 1
+    met.requests_to = np.asarray(ref_counts, np.int64).copy()
+    met.requests_sent = int(met.requests_to.sum())
+    rcounts = _a2a_counts(counts, group, device)                                            # 2
+    recv_ids = torch.empty(int(rcounts.sum()), dtype=torch.int32, device=device)
+    dist.all_to_all_single(recv_ids, req_ids.to(device, torch.int32), output_split_sizes=rcounts.tolist(),
+                           input_split_sizes=counts.tolist(), group=group)
+    recv_mult = torch.empty(int(rcounts.sum()), dtype=torch.int64, device=device)
+    dist.all_to_all_single(recv_mult, req_mult.to(device, torch.int64), output_split_sizes=rcounts.tolist(),
+                           input_split_sizes=counts.tolist(), group=group)
+
+    lens, ids = ops.pack(shard, recv_ids)                                                   # 3
+    lens_np = np.asarray(lens.cpu() if isinstance(lens, torch.Tensor) else lens, np.int64)
+    mult_np = recv_mult.cpu().numpy()
+    met.data_msgs_to = _split_sums(mult_np, rcounts)
+    met.data_msgs_sent = int(met.data_msgs_to.sum())
+    met.completion_msgs_sent = P - 1
+    reply_words = int((mult_np * (2 + lens_np)).sum()) if lens_np.size else 0
+    met.bytes_sent = WORD_BYTES * (2 * met.requests_sent + reply_words + (P - 1))
+    reply_id_counts = _split_sums(lens_np, rcounts)
+    fetched_id_counts = _a2a_counts(reply_id_counts, group, device)
+    fetched_len = torch.empty(int(counts.sum()), dtype=torch.int64, device=device)
+    dist.all_to_all_single(fetched_len, torch.as_tensor(lens_np).to(device), output_split_sizes=counts.tolist(),
+                           input_split_sizes=rcounts.tolist(), group=group)
+    fetched_ids = torch.empty(int(fetched_id_counts.sum()), dtype=torch.int32, device=device)
+    send_ids = ids if isinstance(ids, torch.Tensor) else torch.as_tensor(ids)
+    dist.all_to_all_single(fetched_ids, send_ids.to(device, torch.int32),
+                           output_split_sizes=fetched_id_counts.tolist(),
+                           input_split_sizes=reply_id_counts.tolist(), group=group)
+    met.wire_bytes = int(12 * counts.sum() + 8 * rcounts.sum() + 4 * reply_id_counts.sum() + 16 * P)
+
+    part = ops.count_direct(shard, req_ids, fetched_len, fetched_ids)                       # 4
+    met.triangles = int(part)
+    t = torch.tensor([int(part)], dtype=torch.int64, device=device)
+    dist.all_reduce(t, group=group)                                                         # 5
+    return int(t.item()), met
+
+
+def count_space_direct_dist(g, cost=None, group=None, ops=None):
+    """Multi-GPU count_space_direct (one rank per GPU): returns (total, this
+    rank's RankMetrics)."""
+    from .partitioning import CostKind, partition_ranges, range_bounds
+
+    cost = cost or CostKind.PRED_SUM
+    P = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bounds = range_bounds(partition_ranges(g, cost, P))
+    shard = shard_of(g, int(bounds[rank]), int(bounds[rank + 1]))
+    return direct_rank(shard, bounds, group=group, ops=ops)
+
+
+def emulate_direct_ranks(g, P, cost=None, ops=None):
+    """direct_rank's steps for all P ranks in one process (buffers passed
+    directly).  Returns (total, [RankMetrics])."""
+    from .partitioning import CostKind, partition_ranges, range_bounds
+
+    cost = cost or CostKind.PRED_SUM
+    ops = ops or DeviceOps()
+    bounds = range_bounds(partition_ranges(g, cost, P))
+    shards = [shard_of(g, int(bounds[r]), int(bounds[r + 1])) for r in range(P)]
+    mets = [RankMetrics(rank=r, nranks=P) for r in range(P)]
+    asks = []
+    for r, sh in enumerate(shards):
+        req_ids, req_mult, counts, ref = ops.requests(sh, bounds, P, r)
+        asks.append((req_ids, req_mult, np.asarray(counts, np.int64)))
+        mets[r].requests_to = np.asarray(ref, np.int64).copy()
+        mets[r].requests_sent = int(mets[r].requests_to.sum())
+        mets[r].partition_bytes = WORD_BYTES * ((sh.hi - sh.lo) + 1 + sh.m)
+        mets[r].completion_msgs_sent = P - 1
+    replies = {}  # (server, client) -> (lens, ids)
+    for j, sh in enumerate(shards):
+        words = 0
+        to = np.zeros(P, np.int64)
+        for i in range(P):
+            ids_i, mult_i, counts_i = asks[i]
+            a = int(counts_i[:j].sum())
+            c = int(counts_i[j])
+            if c == 0:
+                continue
+            lens, lists = ops.pack(sh, ids_i[a: a + c])
+            lens_np = np.asarray(lens.cpu() if isinstance(lens, torch.Tensor) else lens, np.int64)
+            mult_np = np.asarray(mult_i[a: a + c].cpu() if isinstance(mult_i, torch.Tensor) else mult_i[a: a + c],
+                                 np.int64)
+            to[i] = int(mult_np.sum())
+            words += int((mult_np * (2 + lens_np)).sum())
+            replies[(j, i)] = (lens_np, lists)
+        mets[j].data_msgs_to = to
+        mets[j].data_msgs_sent = int(to.sum())
+        mets[j].bytes_sent = WORD_BYTES * (2 * mets[j].requests_sent + words + (P - 1))
+    total = 0
+    for i, sh in enumerate(shards):
+        dev = sh.indptr.device
+        parts = [replies[(j, i)] for j in range(P) if (j, i) in replies]
+        flen = torch.as_tensor(np.concatenate([p[0] for p in parts]) if parts else np.zeros(0, np.int64)).to(dev)
+        fids = (torch.cat([torch.as_tensor(p[1]).to(dev, torch.int32) for p in parts]) if parts
+                else torch.zeros(0, dtype=torch.int32, device=dev))
+        mets[i].triangles = int(ops.count_direct(sh, asks[i][0], flen, fids))
+        total += mets[i].triangles
     return total, mets

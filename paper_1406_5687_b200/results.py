@@ -31,6 +31,10 @@ class RankMetrics:
     data_msgs_to: np.ndarray = None
     requests_to: np.ndarray = None
     task_log: list = field(default_factory=list)
+    # B200 extension (not in the reference): bytes this rank actually moved
+    # through its collectives (the counters above keep the reference's
+    # per-message wire model, runtime.py:139-149).
+    wire_bytes: int = 0
 
     def __post_init__(self):
         if self.data_msgs_to is None:

@@ -1,5 +1,5 @@
 """Counting over non-overlapping node-range partitions with the surrogate
-scheme (mirrors space_efficient.py:1-262 of the reference).
+and the direct schemes (mirrors space_efficient.py:1-262 of the reference).
 
 Each rank owns the forward lists of one consecutive, cost-balanced node
 range (PRED_SUM by default, partitioning.py:139-141).  For an oriented edge
@@ -24,7 +24,7 @@ from . import _lib
 from .graph import Graph
 from .partitioning import CostKind, NodeRange, partition_ranges, range_bounds
 from .results import WORD_BYTES, RankMetrics, RunResult
-from .sequential import count_middle
+from .sequential import count_lowest, count_middle
 
 SCAN_CHUNK = 256  # reference constant (space_efficient.py:43); the device scan has no chunking
 
@@ -139,5 +139,63 @@ def count_space_surrogate(g: Graph, nranks: int, cost: CostKind = CostKind.PRED_
         m.bytes_sent = WORD_BYTES * (int(words[r]) + (nranks - 1))
         m.partition_bytes = _partition_bytes(ip, int(bounds[r]), int(bounds[r + 1]))
         metrics.append(m)
+    total = int(partials.sum())
+    return total, RunResult(results=[total] + [None] * (nranks - 1), metrics=metrics, wall=wall)
+
+
+def direct_census(g: Graph, bounds_dev, P):
+    """(requests[P,P], reply_words[P]) of the direct scheme's per-pair
+    messages (space_efficient.py:207-213, runtime.py:139-149)."""
+    dev = g.eff_indptr.device
+    req = torch.empty(P * P, dtype=torch.int64, device=dev)
+    words = torch.empty(P, dtype=torch.int64, device=dev)
+    _lib.call("tc_direct_census", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), g.n, _lib.ptr(bounds_dev),
+              int(P), _lib.ptr(req), _lib.ptr(words), _lib.stream())
+    return req.view(P, P).cpu().numpy(), words.cpu().numpy()
+
+
+def direct_metrics(r, P, partial, req, words, pbytes):
+    """RankMetrics of rank r under the reference's direct-scheme accounting:
+    one 2-word TASK_REQUEST per cross pair, one (2 + d^_u)-word DATA reply
+    per request served, P-1 completion notifiers (space_efficient.py:188-231)."""
+    m = RankMetrics(rank=r, nranks=P)
+    m.triangles = int(partial)
+    m.requests_to = np.asarray(req[r], np.int64).copy()
+    m.requests_sent = int(m.requests_to.sum())
+    m.data_msgs_to = np.asarray(req[:, r], np.int64).copy()
+    m.data_msgs_sent = int(m.data_msgs_to.sum())
+    m.completion_msgs_sent = P - 1
+    m.bytes_sent = WORD_BYTES * (2 * m.requests_sent + int(words[r]) + (P - 1))
+    m.partition_bytes = int(pbytes)
+    return m
+
+
+def count_space_direct(g: Graph, nranks: int, cost: CostKind = CostKind.PRED_SUM, *, backend="det", seed=0,
+                       trace=None):
+    """Exact triangle count with the direct request/response scheme
+    (space_efficient.py:234-262).
+
+    Returns (total, RunResult).  A rank's `triangles` is the lowest-vertex
+    count of its range (the owner of v intersects N^_v with every fetched
+    N^_u, space_efficient.py:206-219), its `requests_to` / `data_msgs_to` /
+    `bytes_sent` follow the reference's one-request-per-cross-pair model.
+    This single-device form evaluates every rank on one GPU; see
+    distributed.count_space_direct_dist for one rank per GPU (deduplicated
+    rank-level pull over NCCL)."""
+    ranges = partition_ranges(g, cost, nranks)
+    bounds = range_bounds(ranges)
+    dev = g.eff_indptr.device
+    bd = torch.as_tensor(bounds).to(dev)
+    t0 = time.perf_counter()
+    if g.n >= 3:
+        partials = count_lowest(g, 0, g.n, bounds=bd).cpu().numpy()
+    else:
+        partials = np.zeros(nranks, dtype=np.int64)
+    wall = time.perf_counter() - t0
+    req, words = direct_census(g, bd, nranks)
+    ip = g.eff_indptr.cpu().numpy()
+    metrics = [direct_metrics(r, nranks, partials[r], req, words,
+                              _partition_bytes(ip, int(bounds[r]), int(bounds[r + 1])))
+               for r in range(nranks)]
     total = int(partials.sum())
     return total, RunResult(results=[total] + [None] * (nranks - 1), metrics=metrics, wall=wall)

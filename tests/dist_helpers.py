@@ -62,6 +62,36 @@ class NumpyOps:
         return total
 
 
+    # -- direct scheme (space_efficient.py:179-231) --
+    def requests(self, shard, bounds, P, rank):
+        ix = shard.indices.numpy()[: shard.m]
+        rem = ix[ix >= shard.hi]
+        ids, mult = np.unique(rem, return_counts=True)
+        b = np.asarray(bounds, np.int64)
+        owners = np.searchsorted(b, ids, side="right") - 1
+        counts = np.bincount(owners, minlength=P).astype(np.int64)
+        ref = np.bincount(owners, weights=mult, minlength=P).astype(np.int64)
+        return (torch.as_tensor(ids.astype(np.int32)), torch.as_tensor(mult.astype(np.int64)), counts, ref)
+
+    def count_direct(self, shard, req_ids, fetched_len, fetched_ids):
+        ip = shard.indptr.numpy()
+        ix = shard.indices.numpy()
+        lo, hi = shard.lo, shard.hi
+        lists = {}
+        off = 0
+        fids = fetched_ids.numpy()
+        for u, ln in zip(req_ids.tolist(), fetched_len.tolist()):
+            lists[u] = set(fids[off: off + ln].tolist())
+            off += ln
+        for v in range(lo, hi):
+            lists[v] = set(ix[ip[v - lo]: ip[v - lo + 1]].tolist())
+        total = 0
+        for v in range(lo, hi):  # count_node_range(lo, hi), _kernels.py:40-52
+            for u in lists[v]:
+                total += len(lists[v] & lists[u])
+        return total
+
+
 def shard_from_arrays(eff_indptr, eff_indices, lo, hi):
     from paper_1406_5687_b200.distributed import Shard
 

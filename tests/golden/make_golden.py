@@ -114,6 +114,14 @@ def reference_outputs(tc, raw_edges):
             out[f"surr_msgs_{P}"] = np.array([m.data_msgs_sent for m in rr.metrics], np.int64)
             out[f"surr_bytes_{P}"] = np.array([m.bytes_sent for m in rr.metrics], np.int64)
             out[f"surr_pbytes_{P}"] = np.array([m.partition_bytes for m in rr.metrics], np.int64)
+            total_d, rd = tc.count_space_direct(g, P, tc.CostKind.PRED_SUM, backend="par")
+            assert total_d == out["T"][0]
+            out[f"direct_tri_{P}"] = np.array([m.triangles for m in rd.metrics], np.int64)
+            out[f"direct_req_{P}"] = np.stack([m.requests_to for m in rd.metrics])
+            out[f"direct_census_{P}"] = np.stack([m.data_msgs_to for m in rd.metrics])
+            out[f"direct_stats_{P}"] = np.array(
+                [[m.requests_sent, m.data_msgs_sent, m.bytes_sent, m.completion_msgs_sent, m.partition_bytes]
+                 for m in rd.metrics], np.int64)
             out[f"lowest_{P}"] = np.array(
                 [tc.count_task(g, tc.Task(int(bounds[i]), int(bounds[i + 1] - bounds[i])))
                  if bounds[i + 1] > bounds[i] else 0 for i in range(P)], np.int64)
@@ -218,7 +226,7 @@ def known_answers(tc):
     return k
 
 
-def config_summary(tc, raw_edges, with_partials=True):
+def config_summary(tc, raw_edges, with_partials=True, with_direct=False):
     norm = tc.normalize(tc.RawGraph.from_pairs(raw_edges))
     g = tc.build_graph(norm)
     succ = tc.node_costs(g, tc.CostKind.SUCC_SUM)
@@ -238,6 +246,12 @@ def config_summary(tc, raw_edges, with_partials=True):
             out[f"surr_census_{P}"] = np.stack([m.data_msgs_to for m in rr.metrics]).tolist()
             out[f"lowest_{P}"] = [int(tc.count_task(g, tc.Task(int(bounds[i]), int(bounds[i + 1] - bounds[i]))))
                                   for i in range(P)]
+            if with_direct:
+                total_d, rd = tc.count_space_direct(g, P, tc.CostKind.PRED_SUM, backend="par")
+                assert total_d == out["T"]
+                out[f"direct_tri_{P}"] = [int(m.triangles) for m in rd.metrics]
+                out[f"direct_req_{P}"] = np.stack([m.requests_to for m in rd.metrics]).tolist()
+                out[f"direct_bytes_{P}"] = [int(m.bytes_sent) for m in rd.metrics]
     return out
 
 
@@ -260,7 +274,7 @@ def main():
     cfg_path = os.path.join(HERE, "configs.json")
     configs = json.load(open(cfg_path)) if os.path.exists(cfg_path) else {}
     raw1 = gen_twin.er_gnm(16384, 131072, 1).astype(np.int64)
-    configs["cfg1_er_gnm_16384_131072_seed1"] = config_summary(tc, raw1)
+    configs["cfg1_er_gnm_16384_131072_seed1"] = config_summary(tc, raw1, with_direct=True)
     if args.big:
         raw2 = tc.generate_pa(tc.PaParams(1_000_000, 100, seed=1)).edges
         configs["cfg2_pa_1000000_100_seed1"] = config_summary(tc, raw2)

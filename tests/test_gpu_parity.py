@@ -270,6 +270,20 @@ def test_cfg2_full_scale(configs):
         assert total == c["T"]
         assert [m.triangles for m in rr.metrics] == c[f"surr_tri_{P}"]
         assert np.stack([m.data_msgs_to for m in rr.metrics]).tolist() == c[f"surr_census_{P}"]
+    # direct scheme: lowest-vertex partials; the census kernel and the
+    # pull's per-rank request multiplicities are independent computations
+    from paper_1406_5687_b200.distributed import emulate_direct_ranks
+    for P in (2, 8):
+        total, rr = tcb.count_space_direct(g, P)
+        assert total == c["T"]
+        assert [m.triangles for m in rr.metrics] == c[f"lowest_{P}"]
+        total2, mets = emulate_direct_ranks(g, P)
+        assert total2 == c["T"]
+        assert [m.triangles for m in mets] == c[f"lowest_{P}"]
+        for a, b in zip(rr.metrics, mets):
+            assert a.requests_to.tolist() == b.requests_to.tolist()
+            assert a.data_msgs_to.tolist() == b.data_msgs_to.tolist()
+            assert a.bytes_sent == b.bytes_sent
 
 
 def test_rmat_scale_properties():
@@ -467,3 +481,53 @@ def test_export_import_round_trip(tmp_path):
         tcb.export_edge_list(g, path)
         g3 = tcb.build_graph(tcb.normalize(tcb.load_edge_list_path(path)))
         assert tcb.count_triangles_seq(g3) == tcb.count_triangles_seq(g)
+
+
+def _check_direct(mets, case, P):
+    assert [m.triangles for m in mets] == case[f"direct_tri_{P}"].tolist()
+    assert np.array_equal(np.stack([m.requests_to for m in mets]), case[f"direct_req_{P}"])
+    assert np.array_equal(np.stack([m.data_msgs_to for m in mets]), case[f"direct_census_{P}"])
+    st = [[m.requests_sent, m.data_msgs_sent, m.bytes_sent, m.completion_msgs_sent, m.partition_bytes]
+          for m in mets]
+    assert st == case[f"direct_stats_{P}"].tolist()
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_direct_parity(name):
+    """count_space_direct on one device (lowest-vertex engine binned by rank
+    + tc_direct_census) against the reference's count_space_direct."""
+    case = SMALL[name]
+    _, g = graph_of(name)
+    if g.n == 0:
+        return
+    for P in (2, 3, 5, 8):
+        total, rr = tcb.count_space_direct(g, P)
+        assert total == int(case["T"][0])
+        _check_direct(rr.metrics, case, P)
+
+
+@pytest.mark.parametrize("name", ["er_60_0.2_21", "pa_1500_12_3", "sparse_labels", "rmat_s10", "gnm_2000_16000",
+                                  "k9", "star", "tie_break"])
+def test_direct_pull_emulated(name):
+    """The per-rank device kernels of the multi-GPU direct scheme (requests,
+    pack, lookup table, lowest-vertex count), ranks one after another."""
+    from paper_1406_5687_b200.distributed import emulate_direct_ranks
+    case = SMALL[name]
+    _, g = graph_of(name)
+    for P in (2, 3, 5, 8):
+        total, mets = emulate_direct_ranks(g, P)
+        assert total == int(case["T"][0])
+        _check_direct(mets, case, P)
+
+
+def test_direct_cfg1(configs):
+    from paper_1406_5687_b200.distributed import emulate_direct_ranks
+    c = configs["cfg1_er_gnm_16384_131072_seed1"]
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=16384, edges=er_edges(16384, 131072, 1))))
+    for P in (2, 4, 8):
+        for total, mets in (tcb.count_space_direct(g, P)[0:1] + (tcb.count_space_direct(g, P)[1].metrics,),
+                            emulate_direct_ranks(g, P)):
+            assert total == c["T"]
+            assert [m.triangles for m in mets] == c[f"direct_tri_{P}"]
+            assert np.stack([m.requests_to for m in mets]).tolist() == c[f"direct_req_{P}"]
+            assert [m.bytes_sent for m in mets] == c[f"direct_bytes_{P}"]

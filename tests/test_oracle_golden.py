@@ -48,6 +48,13 @@ def test_count_costs_partition_match_reference(name):
         partials, census = O.surrogate(g, bounds)
         assert np.array_equal(partials, case[f"surr_tri_{P}"])
         assert np.array_equal(census, case[f"surr_census_{P}"])
+        dp, dreq, dwords = O.direct(g, bounds)
+        assert np.array_equal(dp, case[f"direct_tri_{P}"])
+        assert np.array_equal(dreq, case[f"direct_req_{P}"])
+        assert np.array_equal(dreq.T, case[f"direct_census_{P}"])
+        st = case[f"direct_stats_{P}"]
+        assert np.array_equal(dreq.sum(1), st[:, 0]) and np.array_equal(dreq.sum(0), st[:, 1])
+        assert np.array_equal(8 * (2 * dreq.sum(1) + dwords + (P - 1)), st[:, 2])
         low = [O.count_node_range(g.eff_indptr, g.eff_indices, bounds[i], bounds[i + 1])
                for i in range(P)]
         assert low == case[f"lowest_{P}"].tolist()
@@ -112,6 +119,11 @@ def test_cfg1_instance(configs):
         partials, census = O.surrogate(g, b)
         assert partials.tolist() == c[f"surr_tri_{P}"]
         assert census.tolist() == c[f"surr_census_{P}"]
+        if f"direct_tri_{P}" in c:
+            dp, dreq, dwords = O.direct(g, b)
+            assert dp.tolist() == c[f"direct_tri_{P}"]
+            assert dreq.tolist() == c[f"direct_req_{P}"]
+            assert (8 * (2 * dreq.sum(1) + dwords + (P - 1))).tolist() == c[f"direct_bytes_{P}"]
 
 
 def test_threaded_tasks_sum_to_total():
