@@ -11,6 +11,7 @@ It imports /root/reference/pkg/src/tricount with a raising greenlet stub
     tests/golden/known.json        frozen known answers (counts, plans, ranges)
     tests/golden/small.npz         per-case reference outputs for small graphs
     tests/golden/configs.json      per-config totals / checksums (cfg1, cfg2)
+    tests/golden/suites_*.csv      the reference bench suites' CSV output
 
 The fixtures are consumed by tests/ on CPU (oracle pinning) and on the GPU
 (parity).  Nothing at test time reads /root/reference.
@@ -255,6 +256,28 @@ def config_summary(tc, raw_edges, with_partials=True, with_direct=False):
     return out
 
 
+def suite_csvs(tc):
+    """CSV output of the reference's bench suites (bench.py:79-145) through
+    its metrics writers (metrics.py:105-119), backend "par"."""
+    import io
+    from tricount import bench as tb
+    from tricount import metrics as tm
+
+    g = tb.pa_graph(2000, 10, 3)
+    label = tb.pa_label(2000, 10, 3)
+    pred, deg = tc.CostKind.PRED_SUM, tc.CostKind.DEGREE
+    recs = tb.bench_strong(g, label, "space-surrogate", [2, 4], pred, "par", 0)
+    recs += tb.bench_strong(g, label, "space-direct", [2, 3], pred, "par", 0)
+    recs += tb.bench_weak(400, 8, "space-surrogate", [1, 2, 3], pred, "par", 1)
+    recs += tb.bench_idle(g, label, 4, deg, 2, "par", 5)
+    recs.append(tb._record("space-surrogate", g, label, 0, pred, "par", 0, "count"))  # error row
+    run = io.StringIO()
+    tm.write_run_csv(recs, run)
+    mem = io.StringIO()
+    tm.write_memory_csv(tb.bench_memory(1500, [4, 8, 12], 4, pred, 2), mem)
+    return run.getvalue(), mem.getvalue()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -270,6 +293,12 @@ def main():
         for key, val in reference_outputs(tc, raw).items():
             arrays[f"{name}/{key}"] = val
     np.savez_compressed(os.path.join(HERE, "small.npz"), **arrays)
+
+    run_csv, mem_csv = suite_csvs(tc)
+    with open(os.path.join(HERE, "suites_run.csv"), "w") as f:
+        f.write(run_csv)
+    with open(os.path.join(HERE, "suites_memory.csv"), "w") as f:
+        f.write(mem_csv)
 
     cfg_path = os.path.join(HERE, "configs.json")
     configs = json.load(open(cfg_path)) if os.path.exists(cfg_path) else {}
