@@ -68,21 +68,22 @@ int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges,
  * Outputs (all caller-allocated):
  *   eff_indptr int64[n+1], eff_indices int32[m]      forward CSR N^_v
  *   relabel, orig_ids, deg, eff_deg  int32[n]
- *   rev_indptr int64[n+1]   predecessors of u (v with u in N^_v), by v
- *   rev_src    int32[m]     the predecessor v
- *   rev_seg    int64[2*m]   (e+1, eff_indptr[v+1]): suffix of N^_v after u
+ *   rev_indptr int64[n+1]   predecessor rows: one entry per v with u in N^_v,
+ *                           in unspecified order (the engine sums over a row)
+ *   rev_seg    int32[2*m]   (e+1, eff_indptr[v+1]) of the edge e = (v, u): the
+ *                           suffix of N^_v after u (m < 2^31 so int32 fits)
  *   rev_cost   int64[n+1]   exclusive prefix over u of the pull-engine cost
  * Asynchronous. */
 int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                    int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                    int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                   int32_t* rev_src, int64_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
+                   int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
 
 /* Full CSR (graph.py:125-127) assembled from the forward and reverse CSRs:
- * row u = predecessors (ascending) then N^_u.  full_indptr int64[n+1],
- * full_indices int32[2m]. */
+ * row u = its neighbours ascending (predecessors, then N^_u).  full_indptr
+ * int64[n+1], full_indices int32[2m].  Synchronises. */
 int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
-                  const int64_t* rev_indptr, const int32_t* rev_src, int64_t n,
+                  const int64_t* rev_indptr, const int32_t* rev_seg, int64_t n,
                   int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream);
 
 /* ---------------------------------------------------------------- count */
@@ -91,25 +92,25 @@ int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
  * lies in [u0, u1), written to out[bucket(u)] (uint64).  bucket_bounds
  * (int64[nbuckets+1], ascending) bins u; NULL with nbuckets==1 sums all.
  * Table lists N^_u come from (tab_indptr, tab_indices) indexed by u;
- * predecessor suffixes are rev_seg pairs indexing `pool` (int32).
+ * predecessor suffixes are rev_seg int32 pairs indexing `pool` (int32).
  * On one GPU pool == eff_indices.  out is overwritten (not accumulated).
  * This is count_node_range(0, n) (_kernels.py:40-52) for the whole range,
  * and the per-rank partials of count_space_surrogate for rank buckets. */
 int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
-                    const int64_t* rev_indptr, const int64_t* rev_seg,
+                    const int64_t* rev_indptr, const int32_t* rev_seg,
                     const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
                     int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, tc_stream_t stream);
 
 /* Generic engine over k "virtual owners": owner x probes the table list
  * N^_{owner_map[x]} (owner_map NULL: identity) with segments
- * segs[row_indptr[x] .. row_indptr[x+1]) (pairs into `pool`); cost_prefix
+ * segs[row_indptr[x] .. row_indptr[x+1]) (int32 pairs into `pool`); cost_prefix
  * int64[k+1] drives the chunk plan.  mode 0 = the paper's schedule (half
  * the cost in one chunk per warp, then geometric), mode 1 = owner-ordered
  * uniform chunks then a geometric tail (for L2-tiled owners).  Buckets bin
  * owner_map[x].  out is overwritten. */
 int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
-                    const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                    const int64_t* row_indptr, const int32_t* segs, const int64_t* cost_prefix,
                     const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, int32_t mode, tc_stream_t stream);
 
@@ -117,12 +118,12 @@ int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const
  * into tiles of <= tile_ids list entries and entries are ordered
  * (tile(v), u, v); each (tile, u) with entries is one virtual owner.
  * Outputs (capacity E = rev_indptr[u1] - rev_indptr[u0]): owner_u int32[E],
- * owner_ptr int64[E+1], segs int64[2E], cost_prefix int64[E+1]; returns the
+ * owner_ptr int64[E+1], segs int32[2E], cost_prefix int64[E+1]; returns the
  * owner count k and the tile count.  Feed to tc_count_owners (mode 1).
  * Synchronises. */
 int tc_tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
-                 const int32_t* rev_src, const int64_t* rev_seg, int64_t u0, int64_t u1,
-                 int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int64_t* segs,
+                 const int32_t* rev_seg, int64_t u0, int64_t u1,
+                 int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int32_t* segs,
                  int64_t* cost_prefix, int64_t* k_host, int64_t* ntiles_host, tc_stream_t stream);
 
 /* Lowest-vertex ("push") engine: count_node_range(v0, v1)
@@ -209,18 +210,19 @@ int tc_surrogate_pack(const int64_t* eff_indptr, const int32_t* eff_indices,
  * _kernels.py:70-80, re-expressed): for list l = ids[off[l], off[l+1]) and
  * every position k holding an owned id u in [lo, hi) with a non-empty
  * suffix, emits owner[i] = u - lo and segs[2i..2i+1] =
- * (pool_base + k + 1, pool_base + off[l+1]).  Works for the local shard's
- * own rows and for received lists alike.  owner == NULL only counts.
+ * (pool_base + k + 1, pool_base + off[l+1]) as int32 (the pool must stay
+ * below 2^31 ids).  Works for the local shard's own rows and for received
+ * lists alike.  owner == NULL only counts.
  * Synchronises (returns the segment count; order is unspecified). */
 int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int64_t nl,
-                      int64_t lo, int64_t hi, int64_t pool_base, int32_t* owner, int64_t* segs,
+                      int64_t lo, int64_t hi, int64_t pool_base, int32_t* owner, int32_t* segs,
                       int64_t cap, int64_t* nseg_host, tc_stream_t stream);
 
 /* Groups segments by owner into a CSR usable by tc_count_middle:
- * row_indptr int64[n_owner+1], row_segs int64[2*nseg], cost_prefix
+ * row_indptr int64[n_owner+1], row_segs int32[2*nseg], cost_prefix
  * int64[n_owner+1] (pull-engine cost, needs the table CSR tab_indptr). */
-int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int64_t n_owner,
-                    const int64_t* tab_indptr, int64_t* row_indptr, int64_t* row_segs,
+int tc_segments_csr(const int32_t* owner, const int32_t* segs, int64_t nseg, int64_t n_owner,
+                    const int64_t* tab_indptr, int64_t* row_indptr, int32_t* row_segs,
                     int64_t* cost_prefix, tc_stream_t stream);
 
 /* ------------------------------------------------------------ direct scheme */

@@ -26,12 +26,12 @@ _SIGS = {
     "tc_abi_version": [],
     "tc_trim_pool": [],
     "tc_normalize": [_vp, _i64, _vp, _pi64, _pi64, _vp],
-    "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "tc_build_full": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_count_owners": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp],
-    "tc_tile_pull": [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
+    "tc_tile_pull": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "tc_intersect_count": [_vp, _i64, _vp, _i64, _vp, _vp],
     "tc_engine_timing": [_i32, _vp, _vp, _vp],
     "tc_set_tuning": [_i32, _i64],

@@ -152,43 +152,45 @@ struct RowHi {  // row of a packed (lo << b | hi) key = lo
   int b;
   __device__ int64_t operator()(int64_t i) const { return (int64_t)(k[i] >> b); }
 };
-struct RowU32 {
-  const uint32_t* k;
-  __device__ int64_t operator()(int64_t i) const { return (int64_t)k[i]; }
-};
 
 __global__ void k_eff_indices(const unsigned long long* __restrict__ keys, int64_t m, int b,
-                              int32_t* eff_indices, uint32_t* hi_out) {
+                              int32_t* eff_indices) {
   unsigned long long mask = (1ull << b) - 1;
-  GRID_STRIDE(i, m) {
-    uint32_t hi = (uint32_t)(keys[i] & mask);
-    eff_indices[i] = (int32_t)hi;
-    hi_out[i] = hi;
-  }
+  GRID_STRIDE(i, m) eff_indices[i] = (int32_t)(keys[i] & mask);
 }
 
+// deg / eff_deg of the canonical nodes, and the in-degree (number of
+// predecessors, = deg - eff_deg) that sizes the reverse CSR rows.
 __global__ void k_degrees(const int64_t* __restrict__ indptr, const int32_t* __restrict__ deg_orig,
                           const int32_t* __restrict__ orig_ids, int64_t n, int32_t* deg,
-                          int32_t* eff_deg) {
+                          int32_t* eff_deg, int64_t* in_deg) {
   GRID_STRIDE(v, n) {
-    eff_deg[v] = (int32_t)(indptr[v + 1] - indptr[v]);
-    deg[v] = deg_orig[orig_ids[v]];
+    const int32_t ed = (int32_t)(indptr[v + 1] - indptr[v]);
+    const int32_t d = deg_orig[orig_ids[v]];
+    eff_deg[v] = ed;
+    deg[v] = d;
+    in_deg[v] = d - ed;
   }
 }
 
-__global__ void k_rev_fill(const int32_t* __restrict__ rev_e, const unsigned long long* __restrict__ keys,
-                           int b, const int64_t* __restrict__ eff_indptr, int64_t m,
-                           int32_t* rev_src, longlong2* rev_seg) {
-  GRID_STRIDE(j, m) {
-    int64_t e = rev_e[j];
-    int64_t v = (int64_t)(keys[e] >> b);
-    rev_src[j] = (int32_t)v;
-    rev_seg[j] = make_longlong2(e + 1, eff_indptr[v + 1]);
+// Reverse CSR by counting scatter: edge i = (v, u) of the forward list
+// (keys sorted by (v, u)) goes to a slot of row u claimed with an atomic
+// cursor.  Row order is therefore unspecified -- the pull engine only sums
+// over a row -- and the full CSR sorts its rows when it is assembled.
+__global__ void k_rev_scatter(const unsigned long long* __restrict__ keys, int64_t m, int b,
+                              const int64_t* __restrict__ eff_indptr, const int64_t* __restrict__ rev_indptr,
+                              int32_t* cursor, int2* rev_seg) {
+  const unsigned long long mask = (1ull << b) - 1;
+  GRID_STRIDE(i, m) {
+    const unsigned long long k = keys[i];
+    const int64_t v = (int64_t)(k >> b), u = (int64_t)(k & mask);
+    const int64_t slot = rev_indptr[u] + atomicAdd(&cursor[u], 1);
+    rev_seg[slot] = make_int2((int)(i + 1), (int)eff_indptr[v + 1]);
   }
 }
 
 // Warp per u: pull-engine cost of u (see kSegCost / kTabCost).
-__global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const longlong2* __restrict__ rev_seg,
+__global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const int2* __restrict__ rev_seg,
                            const int64_t* __restrict__ eff_indptr, int64_t n, int64_t* cost) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -199,7 +201,7 @@ __global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const longlon
     long long s = 0;
     if (d > 0)
       for (int64_t r = r0 + lane; r < r1; r += 32) {
-        longlong2 sg = rev_seg[r];
+        const int2 sg = rev_seg[r];
         s += (sg.y - sg.x) + kSegCost;
       }
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -207,9 +209,10 @@ __global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const longlon
   }
 }
 
-// full CSR row u = predecessors (rev_src, ascending) then N^_u.
+// full CSR row u = predecessors (the row of each rev_seg's edge) then N^_u;
+// rows are sorted afterwards.
 __global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
-                       const int64_t* __restrict__ rev_indptr, const int32_t* __restrict__ rev_src,
+                       const int64_t* __restrict__ rev_indptr, const int2* __restrict__ rev_seg,
                        int64_t n, int64_t* full_indptr, int32_t* full_indices) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -219,7 +222,8 @@ __global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __
     if (lane == 0) full_indptr[u] = base;
     if (u == n) continue;
     int64_t r0 = rev_indptr[u], r1 = rev_indptr[u + 1];
-    for (int64_t r = r0 + lane; r < r1; r += 32) full_indices[base + (r - r0)] = rev_src[r];
+    for (int64_t r = r0 + lane; r < r1; r += 32)
+      full_indices[base + (r - r0)] = (int32_t)row_of_edge(eff_indptr, n, (int64_t)rev_seg[r].x - 1);
     int64_t e0 = eff_indptr[u], e1 = eff_indptr[u + 1];
     int64_t off = base + (r1 - r0);
     for (int64_t e = e0 + lane; e < e1; e += 32) full_indices[off + (e - e0)] = eff_indices[e];
@@ -381,8 +385,8 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
 
 void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                  int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel, int32_t* orig_ids,
-                 int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr, int32_t* rev_src,
-                 int64_t* rev_seg, int64_t* rev_cost, cudaStream_t s) {
+                 int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr, int32_t* rev_seg,
+                 int64_t* rev_cost, cudaStream_t s) {
   TC_REQUIRE(n >= 0 && m >= 0, TC_EINVAL, "negative size");
   TC_REQUIRE(n < (1ll << 31) - 1, TC_EINVAL, "n must fit int32 ids");
   TC_REQUIRE(m < (1ll << 31) - 1, TC_EINVAL, "m must be < 2^31");
@@ -438,34 +442,33 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   }
   unsigned long long* keys = sort_keys(sc, ka, kb, m, 2 * b, s);
   indptr_from_sorted(sc, RowHi{keys, b}, m, n, eff_indptr, s);
-  uint32_t* hi = sc.alloc<uint32_t>(m);
-  uint32_t* hi2 = sc.alloc<uint32_t>(m);
   if (m) {
-    k_eff_indices<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indices, hi);
+    k_eff_indices<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indices);
     check_launch();
   }
-  k_degrees<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, deg_orig, orig_ids, n, deg, eff_deg);
+  int64_t* in_deg = sc.alloc<int64_t>(n + 1);
+  TC_CUDA(cudaMemsetAsync(in_deg + n, 0, sizeof(int64_t), s));
+  k_degrees<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, deg_orig, orig_ids, n, deg, eff_deg, in_deg);
   check_launch();
 
-  // reverse CSR: predecessors of u sorted by v (stable sort by hi of the
-  // lo-sorted edge list), each with the suffix of N^_v after u.
-  int32_t* re = sc.alloc<int32_t>(m);
-  int32_t* re2 = sc.alloc<int32_t>(m);
-  if (m) {
-    k_iota<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(re, m);
-    check_launch();
+  // reverse CSR: predecessors of u, each with the suffix of N^_v after u
+  {
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in_deg, rev_indptr, n + 1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in_deg, rev_indptr, n + 1, s));
   }
-  sort_pairs(sc, hi, hi2, re, re2, m, b, s);
-  indptr_from_sorted(sc, RowU32{hi}, m, n, rev_indptr, s);
   if (m) {
-    k_rev_fill<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(re, keys, b, eff_indptr, m, rev_src,
-                                                                reinterpret_cast<longlong2*>(rev_seg));
+    int32_t* cursor = sc.alloc<int32_t>(n);
+    TC_CUDA(cudaMemsetAsync(cursor, 0, n * sizeof(int32_t), s));
+    k_rev_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indptr, rev_indptr, cursor,
+                                                                   reinterpret_cast<int2*>(rev_seg));
     check_launch();
   }
   // pull-engine cost prefix over u
   int64_t* cu = sc.alloc<int64_t>(n + 1);
   k_rev_cost<<<grid_for(n * 32, kBlock, sms * 16), kBlock, 0, s>>>(
-      rev_indptr, reinterpret_cast<const longlong2*>(rev_seg), eff_indptr, n, cu);
+      rev_indptr, reinterpret_cast<const int2*>(rev_seg), eff_indptr, n, cu);
   check_launch();
   TC_CUDA(cudaMemsetAsync(cu + n, 0, sizeof(int64_t), s));
   {
@@ -542,22 +545,41 @@ int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_
 int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                    int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                    int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                   int32_t* rev_src, int64_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
+                   int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
   return tcb::guarded([&] {
     tcb::build_graph(edges, m, n, order, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
-                     rev_indptr, rev_src, rev_seg, rev_cost, (cudaStream_t)stream);
+                     rev_indptr, rev_seg, rev_cost, (cudaStream_t)stream);
   });
 }
 
 int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
-                  const int64_t* rev_indptr, const int32_t* rev_src, int64_t n,
+                  const int64_t* rev_indptr, const int32_t* rev_seg, int64_t n,
                   int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream) {
   return tcb::guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
     int sms = tcb::sm_count();
+    int64_t m2 = 0;
+    {
+      int64_t a = 0, b = 0;
+      TC_CUDA(cudaMemcpyAsync(&a, eff_indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      TC_CUDA(cudaMemcpyAsync(&b, rev_indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      tcb::sync_stream(s);
+      m2 = a + b;
+    }
+    tcb::Scratch sc(s);
+    int32_t* unsorted = sc.alloc<int32_t>(m2 > 0 ? m2 : 1);
     tcb::k_full<<<tcb::grid_for((n + 1) * 32, 256, sms * 16), 256, 0, s>>>(
-        eff_indptr, eff_indices, rev_indptr, rev_src, n, full_indptr, full_indices);
+        eff_indptr, eff_indices, rev_indptr, reinterpret_cast<const int2*>(rev_seg), n, full_indptr, unsorted);
     tcb::check_launch();
+    if (m2 > 0) {  // predecessor rows are unordered (k_rev_scatter): sort every row
+      TC_REQUIRE(m2 < (1ll << 31), TC_EINVAL, "full CSR too large");
+      size_t tmp = 0;
+      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, unsorted, full_indices, (int)m2, (int)n,
+                                                 full_indptr, full_indptr + 1, s));
+      void* t = sc.bytes(tmp);
+      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(t, tmp, unsorted, full_indices, (int)m2, (int)n, full_indptr,
+                                                 full_indptr + 1, s));
+    }
   });
 }
 

@@ -103,6 +103,17 @@ inline void check_launch() {
   TC_CUDA(cudaGetLastError());
 }
 
+// Row of forward edge e: the largest v with indptr[v] <= e (indptr[n] = m > e).
+__device__ __forceinline__ int64_t row_of_edge(const int64_t* __restrict__ indptr, int64_t n, int64_t e) {
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(&indptr[mid]) <= e) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 }  // namespace tcb
 
 #define GRID_STRIDE(i, n) \

@@ -81,10 +81,10 @@ struct WarpSliceT {
 
 // --------------------------------------------------------------- segments
 
-struct PullSegs {  // rev_seg pairs (start, end) into the pool
-  const longlong2* seg;
+struct PullSegs {  // rev_seg int32 pairs (start, end) into the pool
+  const int2* seg;
   __device__ __forceinline__ void get(int64_t r, int64_t& s, int64_t& e) const {
-    longlong2 x = __ldg(&seg[r]);
+    const int2 x = __ldg(&seg[r]);
     s = x.x;
     e = x.y;
   }
@@ -978,7 +978,7 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
 }
 
 void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                  const int64_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n,
+                  const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n,
                   int64_t u0, int64_t u1, const int64_t* bucket_bounds, int nbuckets,
                   unsigned long long* out, cudaStream_t s) {
   TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
@@ -989,11 +989,11 @@ void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const i
   if (u1 <= u0) return;
   Scratch sc(s);
   run_engine(sc, n, rev_cost, rev_indptr, tab_indptr, tab_indices, pool, u0, u1, bucket_bounds,
-             nbuckets, out, PullSegs{reinterpret_cast<const longlong2*>(rev_seg)}, s, nullptr, 1);
+             nbuckets, out, PullSegs{reinterpret_cast<const int2*>(rev_seg)}, s, nullptr, 1);
 }
 
 void count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
-                  const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                  const int64_t* row_indptr, const int32_t* segs, const int64_t* cost_prefix,
                   const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int nbuckets,
                   unsigned long long* out, int mode, cudaStream_t s) {
   TC_REQUIRE(k >= 0 && nbuckets >= 1, TC_EINVAL, "bad owner count / nbuckets");
@@ -1003,7 +1003,7 @@ void count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const i
   if (k == 0) return;
   Scratch sc(s);
   run_engine(sc, k, cost_prefix, row_indptr, tab_indptr, tab_indices, pool, 0, k, bucket_bounds,
-             nbuckets, out, PullSegs{reinterpret_cast<const longlong2*>(segs)}, s, owner_map, mode);
+             nbuckets, out, PullSegs{reinterpret_cast<const int2*>(segs)}, s, owner_map, mode);
 }
 
 void count_lowest(const int64_t* indptr, const int32_t* indices, int64_t n, int64_t v0, int64_t v1,
@@ -1077,7 +1077,7 @@ __global__ void k_brute_count(const uint32_t* __restrict__ adj, int64_t n, int64
 extern "C" {
 
 int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
-                    const int64_t* rev_indptr, const int64_t* rev_seg, const int64_t* rev_cost,
+                    const int64_t* rev_indptr, const int32_t* rev_seg, const int64_t* rev_cost,
                     const int32_t* pool, int64_t n, int64_t u0, int64_t u1,
                     const int64_t* bucket_bounds, int32_t nbuckets, unsigned long long* out,
                     tc_stream_t stream) {
@@ -1088,7 +1088,7 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
 }
 
 int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
-                    const int64_t* row_indptr, const int64_t* segs, const int64_t* cost_prefix,
+                    const int64_t* row_indptr, const int32_t* segs, const int64_t* cost_prefix,
                     const int32_t* pool, int64_t k, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, int32_t mode, tc_stream_t stream) {
   return tcb::guarded([&] {

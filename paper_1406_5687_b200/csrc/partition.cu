@@ -270,7 +270,7 @@ __global__ void k_pack(const int64_t* __restrict__ indptr, const int32_t* __rest
 __global__ void k_owner_segs(const int64_t* __restrict__ off, const int32_t* __restrict__ ids,
                              int64_t nl, int64_t lo, int64_t hi, int64_t pool_base,
                              unsigned long long* counter, int64_t cap, int32_t* owner,
-                             longlong2* segs) {
+                             int2* segs) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -289,14 +289,14 @@ __global__ void k_owner_segs(const int64_t* __restrict__ off, const int32_t* __r
         int64_t slot = (int64_t)base + __popc(m & ((1u << lane) - 1));
         if (owner && slot < cap) {
           owner[slot] = (int32_t)(u - lo);
-          segs[slot] = make_longlong2(pool_base + k + 1, pool_base + b);
+          segs[slot] = make_int2((int)(pool_base + k + 1), (int)(pool_base + b));
         }
       }
     }
   }
 }
 
-__global__ void k_seg_cost_rows(const int64_t* __restrict__ row, const longlong2* __restrict__ segs,
+__global__ void k_seg_cost_rows(const int64_t* __restrict__ row, const int2* __restrict__ segs,
                                 const int64_t* __restrict__ tab_indptr, int64_t n, int64_t* cost) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -328,8 +328,8 @@ struct RowI32 {
 __global__ void k_iota64(int64_t* a, int64_t n) {
   GRID_STRIDE(i, n) a[i] = i;
 }
-__global__ void k_gather_segs(const longlong2* __restrict__ in, const int64_t* __restrict__ idx,
-                              int64_t n, longlong2* out) {
+__global__ void k_gather_segs(const int2* __restrict__ in, const int64_t* __restrict__ idx,
+                              int64_t n, int2* out) {
   GRID_STRIDE(i, n) out[i] = in[idx[i]];
 }
 
@@ -443,7 +443,7 @@ int tc_surrogate_pack(const int64_t* eff_indptr, const int32_t* eff_indices, con
 }
 
 int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int64_t nl, int64_t lo,
-                      int64_t hi, int64_t pool_base, int32_t* owner, int64_t* segs, int64_t cap,
+                      int64_t hi, int64_t pool_base, int32_t* owner, int32_t* segs, int64_t cap,
                       int64_t* nseg_host, tc_stream_t stream) {
   return tcb::guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
@@ -452,9 +452,13 @@ int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int6
     TC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
     *nseg_host = 0;
     if (nl <= 0) return;
+    int64_t last = 0;
+    TC_CUDA(cudaMemcpyAsync(&last, list_offsets + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    tcb::sync_stream(s);
+    TC_REQUIRE(pool_base >= 0 && pool_base + last < (1ll << 31), TC_EINVAL, "segment pool must stay below 2^31 ids");
     tcb::k_owner_segs<<<tcb::grid_for(nl * 32, 256, tcb::sm_count() * 16), 256, 0, s>>>(
         list_offsets, list_ids, nl, lo, hi, pool_base, ctr, cap, owner,
-        reinterpret_cast<longlong2*>(segs));
+        reinterpret_cast<int2*>(segs));
     tcb::check_launch();
     unsigned long long c = tcb::read_scalar(ctr, s);
     *nseg_host = (int64_t)c;
@@ -462,8 +466,8 @@ int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int6
   });
 }
 
-int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int64_t n_owner,
-                    const int64_t* tab_indptr, int64_t* row_indptr, int64_t* row_segs,
+int tc_segments_csr(const int32_t* owner, const int32_t* segs, int64_t nseg, int64_t n_owner,
+                    const int64_t* tab_indptr, int64_t* row_indptr, int32_t* row_segs,
                     int64_t* cost_prefix, tc_stream_t stream) {
   return tcb::guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
@@ -486,7 +490,7 @@ int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int
       k1 = k.Current();
       i1 = v.Current();
       tcb::k_gather_segs<<<tcb::grid_for(nseg, 256), 256, 0, s>>>(
-          reinterpret_cast<const longlong2*>(segs), i1, nseg, reinterpret_cast<longlong2*>(row_segs));
+          reinterpret_cast<const int2*>(segs), i1, nseg, reinterpret_cast<int2*>(row_segs));
       tcb::check_launch();
     }
     long long* cnt = sc.alloc<long long>(n_owner + 1);
@@ -500,7 +504,7 @@ int tc_segments_csr(const int32_t* owner, const int64_t* segs, int64_t nseg, int
     TC_CUDA(cudaMemsetAsync(cost + n_owner, 0, sizeof(int64_t), s));
     if (n_owner) {
       tcb::k_seg_cost_rows<<<tcb::grid_for(n_owner * 32, 256, tcb::sm_count() * 16), 256, 0, s>>>(
-          row_indptr, reinterpret_cast<const longlong2*>(row_segs), tab_indptr, n_owner, cost);
+          row_indptr, reinterpret_cast<const int2*>(row_segs), tab_indptr, n_owner, cost);
       tcb::check_launch();
     }
     tcb::exclusive_sum(sc, cost, cost_prefix, n_owner + 1, s);

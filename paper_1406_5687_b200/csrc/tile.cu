@@ -45,11 +45,12 @@ __global__ void k_entry_u(const int64_t* __restrict__ rev_indptr, int64_t u0, in
     for (int64_t j = rev_indptr[u] + lane; j < rev_indptr[u + 1]; j += 32) uarr[j - r0] = (int32_t)u;
 }
 
-__global__ void k_tile_keys(const int32_t* __restrict__ rev_src, const int32_t* __restrict__ uarr, int64_t r0,
+__global__ void k_tile_keys(const int2* __restrict__ rev_seg, const int64_t* __restrict__ eff_indptr, int64_t n,
+                            const int32_t* __restrict__ uarr, int64_t r0,
                             int64_t E, const int64_t* __restrict__ vt, int T, int64_t u0, int bu,
                             unsigned long long* keys, int32_t* vals) {
   GRID_STRIDE(i, E) {
-    int64_t v = rev_src[r0 + i];
+    int64_t v = row_of_edge(eff_indptr, n, (int64_t)rev_seg[r0 + i].x - 1);
     int lo = 0, hi = T;  // largest t with vt[t] <= v
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
@@ -78,13 +79,13 @@ __global__ void k_owner_emit(const unsigned long long* __restrict__ keys, const 
   }
 }
 
-__global__ void k_gather_tseg(const longlong2* __restrict__ rev_seg, int64_t r0, const int32_t* __restrict__ vals,
-                              int64_t E, longlong2* segs) {
+__global__ void k_gather_tseg(const int2* __restrict__ rev_seg, int64_t r0, const int32_t* __restrict__ vals,
+                              int64_t E, int2* segs) {
   GRID_STRIDE(i, E) segs[i] = rev_seg[r0 + vals[i]];
 }
 
 __global__ void k_owner_cost(const int64_t* __restrict__ owner_ptr, const int32_t* __restrict__ owner_u,
-                             const longlong2* __restrict__ segs, const int64_t* __restrict__ eff_indptr,
+                             const int2* __restrict__ segs, const int64_t* __restrict__ eff_indptr,
                              int64_t K, int64_t* cost) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -108,9 +109,9 @@ static void excl_sum(Scratch& sc, In in, Out out, int64_t n, cudaStream_t s) {
   TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, s));
 }
 
-static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr, const int32_t* rev_src,
-                      const int64_t* rev_seg, int64_t u0, int64_t u1, int64_t tile_ids, int32_t* owner_u,
-                      int64_t* owner_ptr, int64_t* segs, int64_t* cost_prefix, int64_t* k_host,
+static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
+                      const int32_t* rev_seg, int64_t u0, int64_t u1, int64_t tile_ids, int32_t* owner_u,
+                      int64_t* owner_ptr, int32_t* segs, int64_t* cost_prefix, int64_t* k_host,
                       int64_t* ntiles_host, cudaStream_t s) {
   TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
   TC_REQUIRE(tile_ids >= 1, TC_EINVAL, "tile_ids must be >= 1");
@@ -143,7 +144,7 @@ static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_i
   auto* kb = sc.alloc<unsigned long long>(E);
   int32_t* va = sc.alloc<int32_t>(E);
   int32_t* vb = sc.alloc<int32_t>(E);
-  k_tile_keys<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(rev_src, uarr, r0, E, vt, T, u0, bu, ka, va);
+  k_tile_keys<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(reinterpret_cast<const int2*>(rev_seg), eff_indptr, n, uarr, r0, E, vt, T, u0, bu, ka, va);
   check_launch();
   {
     cub::DoubleBuffer<unsigned long long> dk(ka, kb);
@@ -168,13 +169,13 @@ static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_i
   k_owner_emit<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(ka, flag, idx, E, u0, bu, owner_u, owner_ptr);
   check_launch();
   TC_CUDA(cudaMemcpyAsync(owner_ptr + K, &E, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  k_gather_tseg<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(reinterpret_cast<const longlong2*>(rev_seg), r0, va, E,
-                                                           reinterpret_cast<longlong2*>(segs));
+  k_gather_tseg<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(reinterpret_cast<const int2*>(rev_seg), r0, va, E,
+                                                           reinterpret_cast<int2*>(segs));
   check_launch();
   int64_t* cost = sc.alloc<int64_t>(K + 1);
   TC_CUDA(cudaMemsetAsync(cost + K, 0, sizeof(int64_t), s));
   k_owner_cost<<<grid_for(K * 32, 256, sms * 16), 256, 0, s>>>(owner_ptr, owner_u,
-                                                               reinterpret_cast<const longlong2*>(segs),
+                                                               reinterpret_cast<const int2*>(segs),
                                                                eff_indptr, K, cost);
   check_launch();
   excl_sum(sc, cost, cost_prefix, K + 1, s);
@@ -185,11 +186,11 @@ static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_i
 }  // namespace tcb
 
 extern "C" int tc_tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
-                            const int32_t* rev_src, const int64_t* rev_seg, int64_t u0, int64_t u1,
-                            int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int64_t* segs,
+                            const int32_t* rev_seg, int64_t u0, int64_t u1,
+                            int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int32_t* segs,
                             int64_t* cost_prefix, int64_t* k_host, int64_t* ntiles_host, tc_stream_t stream) {
   return tcb::guarded([&] {
-    tcb::tile_pull(eff_indptr, n, rev_indptr, rev_src, rev_seg, u0, u1, tile_ids, owner_u, owner_ptr, segs,
+    tcb::tile_pull(eff_indptr, n, rev_indptr, rev_seg, u0, u1, tile_ids, owner_u, owner_ptr, segs,
                    cost_prefix, k_host, ntiles_host, (cudaStream_t)stream);
   });
 }

@@ -77,14 +77,16 @@ class Graph:
     (graph.py:36-73).  Array fields are torch tensors on the GPU."""
 
     __slots__ = ("n", "m", "eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg",
-                 "_rev_indptr", "_rev_src", "_rev_seg", "_rev_cost", "_full", "_cache")
+                 "_rev_indptr", "_rev_seg", "_rev_cost", "_full", "_cache")
 
     def __init__(self, n, m, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg, rev_indptr,
-                 rev_src, rev_seg, rev_cost):
+                 rev_seg, rev_cost):
         self.n, self.m = int(n), int(m)
         self.eff_indptr, self.eff_indices = eff_indptr, eff_indices
         self.relabel, self.orig_ids, self.deg, self.eff_deg = relabel, orig_ids, deg, eff_deg
-        self._rev_indptr, self._rev_src, self._rev_seg, self._rev_cost = rev_indptr, rev_src, rev_seg, rev_cost
+        # reverse CSR for the pull engine: per u, the (start, end) int32 pairs of
+        # its predecessors' suffixes in eff_indices (rows unordered)
+        self._rev_indptr, self._rev_seg, self._rev_cost = rev_indptr, rev_seg, rev_cost
         self._full = None
         self._cache = {}
 
@@ -95,7 +97,7 @@ class Graph:
             fip = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
             fix = torch.empty(max(2 * self.m, 1), dtype=torch.int32, device=dev)
             _lib.call("tc_build_full", _lib.ptr(self.eff_indptr), _lib.ptr(self.eff_indices),
-                      _lib.ptr(self._rev_indptr), _lib.ptr(self._rev_src), self.n, _lib.ptr(fip),
+                      _lib.ptr(self._rev_indptr), _lib.ptr(self._rev_seg), self.n, _lib.ptr(fip),
                       _lib.ptr(fix), _lib.stream())
             self._full = (fip, fix[: 2 * self.m])
         return self._full
@@ -164,11 +166,11 @@ def tiled_index(g: "Graph", u0: int, u1: int) -> TiledIndex:
         E = int(g._rev_indptr[u1] - g._rev_indptr[u0]) if g.n else 0
         owner_u = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
         owner_ptr = torch.empty(E + 1, dtype=torch.int64, device=dev)
-        segs = torch.empty(max(2 * E, 2), dtype=torch.int64, device=dev)
+        segs = torch.empty(max(2 * E, 2), dtype=torch.int32, device=dev)
         cost = torch.empty(E + 1, dtype=torch.int64, device=dev)
         k, nt = ctypes.c_int64(), ctypes.c_int64()
         if g.n:
-            _lib.call("tc_tile_pull", _lib.ptr(g.eff_indptr), g.n, _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_src),
+            _lib.call("tc_tile_pull", _lib.ptr(g.eff_indptr), g.n, _lib.ptr(g._rev_indptr),
                       _lib.ptr(g._rev_seg), u0, u1, TILE_IDS, _lib.ptr(owner_u), _lib.ptr(owner_ptr),
                       _lib.ptr(segs), _lib.ptr(cost), ctypes.byref(k), ctypes.byref(nt), _lib.stream())
         else:
@@ -205,16 +207,15 @@ def _assemble(raw: RawGraph, order) -> Graph:
     # +4 ids of padding: the engines read lists as 16-byte chunks
     eff_indptr, eff_indices = i64(n + 1), i32(m + 4)
     relabel, orig_ids, deg, eff_deg = i32(n), i32(n), i32(n), i32(n)
-    rev_indptr, rev_src, rev_seg, rev_cost = i64(n + 1), i32(m), i64(2 * m), i64(n + 1)
+    rev_indptr, rev_seg, rev_cost = i64(n + 1), i32(2 * m), i64(n + 1)
     order_t = None
     if order is not None:
         order_t = torch.as_tensor(np.asarray(order, dtype=np.int32)).to(dev).contiguous()
     _lib.call("tc_build_graph", _lib.ptr(e), m, n, _lib.ptr(order_t), _lib.ptr(eff_indptr),
               _lib.ptr(eff_indices), _lib.ptr(relabel), _lib.ptr(orig_ids), _lib.ptr(deg),
-              _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_src), _lib.ptr(rev_seg),
-              _lib.ptr(rev_cost), _lib.stream())
+              _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_seg), _lib.ptr(rev_cost), _lib.stream())
     g = Graph(n, m, eff_indptr[: n + 1], eff_indices[:m], relabel[:n], orig_ids[:n], deg[:n],
-              eff_deg[:n], rev_indptr[: n + 1], rev_src[:m], rev_seg[: 2 * m], rev_cost[: n + 1])
+              eff_deg[:n], rev_indptr[: n + 1], rev_seg[: 2 * m], rev_cost[: n + 1])
     if TILE_IDS:
         tiled_index(g, 0, n)  # optional L2-tiled predecessor index, built with the graph
     return g

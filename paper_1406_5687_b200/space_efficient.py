@@ -71,7 +71,7 @@ def owner_segments(list_offsets, list_ids, lo, hi, pool_base):
     k = cnt.value
     dev = list_ids.device
     owner = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
-    segs = torch.empty(max(2 * k, 2), dtype=torch.int64, device=dev)
+    segs = torch.empty(max(2 * k, 2), dtype=torch.int32, device=dev)
     _lib.call("tc_owner_segments", _lib.ptr(list_offsets), _lib.ptr(list_ids), nl, int(lo), int(hi),
               int(pool_base), _lib.ptr(owner), _lib.ptr(segs), k, ctypes.byref(cnt), _lib.stream())
     return owner, segs, k
@@ -81,7 +81,7 @@ def count_segments(tab_indptr, tab_indices, pool, owner, segs, nseg, n_owner, bo
     """Middle-vertex engine over explicit segments (tables indexed 0..n_owner)."""
     dev = pool.device
     row = torch.empty(n_owner + 1, dtype=torch.int64, device=dev)
-    rsegs = torch.empty(max(2 * nseg, 2), dtype=torch.int64, device=dev)
+    rsegs = torch.empty(max(2 * nseg, 2), dtype=torch.int32, device=dev)
     cost = torch.empty(n_owner + 1, dtype=torch.int64, device=dev)
     tab_indptr = tab_indptr.contiguous()
     _lib.call("tc_segments_csr", _lib.ptr(owner), _lib.ptr(segs), int(nseg), int(n_owner),
