@@ -212,8 +212,9 @@ int tc_surrogate_pack(const int64_t* eff_indptr, const int32_t* eff_indices,
  * suffix, emits owner[i] = u - lo and segs[2i..2i+1] =
  * (pool_base + k + 1, pool_base + off[l+1]) as int32 (the pool must stay
  * below 2^31 ids).  Works for the local shard's own rows and for received
- * lists alike.  owner == NULL only counts.
- * Synchronises (returns the segment count; order is unspecified). */
+ * lists alike.  owner == NULL only counts; otherwise cap >= the number of
+ * ids always suffices.  Segments come in list order, positions ascending.
+ * Synchronises (returns the segment count). */
 int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int64_t nl,
                       int64_t lo, int64_t hi, int64_t pool_base, int32_t* owner, int32_t* segs,
                       int64_t cap, int64_t* nseg_host, tc_stream_t stream);

@@ -45,8 +45,37 @@ struct NotSelfLoop {
   }
 };
 
-__global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t cnt, uint32_t* fp) {
-  GRID_STRIDE(i, cnt) atomicMin(&fp[ids[i]], (uint32_t)i);
+// Run aggregation for scattered atomics: lanes of a warp that hold equal
+// keys in consecutive lanes form a run; the run's last lane gets its length
+// and the lane index where it starts (other lanes get 0).  Sorted or
+// grouped inputs (normalized edge lists, generator output) turn up to 32
+// atomics into one; arbitrary inputs stay correct.
+__device__ __forceinline__ int warp_run_end(int32_t key, bool valid, int lane, int* start) {
+  const int32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const int32_t next = __shfl_down_sync(0xffffffffu, key, 1);
+  const bool vprev = __shfl_up_sync(0xffffffffu, valid, 1);
+  const bool vnext = __shfl_down_sync(0xffffffffu, valid, 1);
+  const bool head = lane == 0 || !vprev || prev != key;
+  const bool tail = lane == 31 || !vnext || next != key;
+  const unsigned heads = __ballot_sync(0xffffffffu, valid && head);
+  if (!valid || !tail) return 0;
+  *start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+  return lane - *start + 1;
+}
+
+// First position of every label in the raveled pair list (thread per pair;
+// the two endpoint columns are aggregated separately).
+__global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t npairs, uint32_t* fp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < npairs;
+    const int2 p = valid ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
+    int st = 0;
+    if (warp_run_end(p.x, valid, lane, &st)) atomicMin(&fp[p.x], (uint32_t)(2 * (i - lane + st)));
+    if (warp_run_end(p.y, valid, lane, &st)) atomicMin(&fp[p.y], (uint32_t)(2 * (i - lane + st) + 1));
+  }
 }
 
 // K = number of present labels, Lf = largest present label.
@@ -91,18 +120,37 @@ __global__ void k_remap(int32_t* ids, int64_t cnt, const int32_t* __restrict__ n
 }
 
 // (min, max) of each pair packed as lo << b | hi; optional relabel map.
+__device__ __forceinline__ unsigned long long pair_key(const int32_t* __restrict__ e, int64_t i,
+                                                     const int32_t* __restrict__ relabel, int b) {
+  int32_t x = e[2 * i], y = e[2 * i + 1];
+  if (relabel) {
+    x = relabel[x];
+    y = relabel[y];
+  }
+  return ((unsigned long long)(uint32_t)min(x, y) << b) | (uint32_t)max(x, y);
+}
+
+// Packs (min, max) keys and records how far the list is from sorted:
+// flags bit 0 = some key decreases, bit 1 = some low half (max endpoint)
+// decreases.  With bit 1 clear the low-half radix passes would be identity
+// permutations, so the sort only needs the high half (e.g. generator output
+// grouped by the newer endpoint); with bit 0 clear it needs nothing.
 __global__ void k_pack_pairs(const int32_t* __restrict__ e, int64_t m,
                              const int32_t* __restrict__ relabel, int b,
-                             unsigned long long* keys) {
+                             unsigned long long* keys, unsigned* order_flags) {
+  const unsigned long long mask = (1ull << b) - 1;
+  unsigned f = 0;
   GRID_STRIDE(i, m) {
-    int32_t x = e[2 * i], y = e[2 * i + 1];
-    if (relabel) {
-      x = relabel[x];
-      y = relabel[y];
+    const unsigned long long k = pair_key(e, i, relabel, b);
+    keys[i] = k;
+    if (order_flags && i > 0) {
+      const unsigned long long p = pair_key(e, i - 1, relabel, b);
+      f |= (k < p ? 1u : 0u) | ((k & mask) < (p & mask) ? 2u : 0u);
     }
-    uint32_t lo = (uint32_t)min(x, y), hi = (uint32_t)max(x, y);
-    keys[i] = ((unsigned long long)lo << b) | hi;
   }
+  if (!order_flags) return;
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(order_flags, f);
 }
 
 __global__ void k_unpack_pairs(const unsigned long long* __restrict__ keys, int64_t m, int b,
@@ -115,8 +163,18 @@ __global__ void k_unpack_pairs(const unsigned long long* __restrict__ keys, int6
   }
 }
 
-__global__ void k_histogram(const int32_t* __restrict__ ids, int64_t cnt, int32_t* h) {
-  GRID_STRIDE(i, cnt) atomicAdd(&h[ids[i]], 1);
+// Degree histogram over the pair list (thread per pair, run-aggregated).
+__global__ void k_histogram(const int32_t* __restrict__ ids, int64_t npairs, int32_t* h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < npairs;
+    const int2 p = valid ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
+    int st = 0, c;
+    if ((c = warp_run_end(p.x, valid, lane, &st))) atomicAdd(&h[p.x], c);
+    if ((c = warp_run_end(p.y, valid, lane, &st))) atomicAdd(&h[p.y], c);
+  }
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -233,14 +291,26 @@ __global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __
 // ---------------------------------------------------------------- sorting
 
 template <class K>
-K* sort_keys(Scratch& sc, K* a, K* b, int64_t n, int end_bit, cudaStream_t s) {
-  if (n <= 1 || end_bit <= 0) return a;
+K* sort_keys(Scratch& sc, K* a, K* b, int64_t n, int end_bit, cudaStream_t s, int begin_bit = 0) {
+  if (n <= 1 || end_bit <= begin_bit) return a;
   cub::DoubleBuffer<K> db(a, b);
   size_t tmp = 0;
-  TC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, n, 0, end_bit, s));
+  TC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, n, begin_bit, end_bit, s));
   void* t = sc.bytes(tmp);
-  TC_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, n, 0, end_bit, s));
+  TC_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, db, n, begin_bit, end_bit, s));
   return db.Current();
+}
+
+// Radix sort of packed (lo << b | hi) keys using the order flags of
+// k_pack_pairs: skip the sort, or sort the high half only (stable LSD
+// passes over an already non-decreasing low half change nothing).
+template <class K>
+K* sort_packed(Scratch& sc, K* a, K* bb, int64_t n, int b, const unsigned* order_flags, cudaStream_t s) {
+  unsigned f = 0;
+  TC_CUDA(cudaMemcpyAsync(&f, order_flags, sizeof(f), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);
+  if (!(f & 1u)) return a;
+  return sort_keys(sc, a, bb, n, 2 * b, s, (f & 2u) ? 0 : b);
 }
 
 template <class K, class V>
@@ -323,7 +393,7 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   // first occurrence of each label in the raveled order (graph.py:92-93)
   uint32_t* fp = sc.alloc<uint32_t>(L1);
   TC_CUDA(cudaMemsetAsync(fp, 0xFF, L1 * sizeof(uint32_t), s));
-  k_first_pos<<<grid_for(nid, kBlock, sms * 16), kBlock, 0, s>>>(ids, nid, fp);
+  k_first_pos<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, fp);
   check_launch();
   auto* cnt = sc.alloc<unsigned long long>(1);
   int* lf = sc.alloc<int>(1);
@@ -363,9 +433,11 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   int b = std::max(1, bits_for((uint64_t)(K - 1)));
   auto* ka = sc.alloc<unsigned long long>(m1);
   auto* kb = sc.alloc<unsigned long long>(m1);
-  k_pack_pairs<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, nullptr, b, ka);
+  unsigned* oflags = sc.alloc<unsigned>(1);
+  TC_CUDA(cudaMemsetAsync(oflags, 0, sizeof(unsigned), s));
+  k_pack_pairs<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, nullptr, b, ka, oflags);
   check_launch();
-  unsigned long long* sorted = sort_keys(sc, ka, kb, m1, 2 * b, s);
+  unsigned long long* sorted = sort_packed(sc, ka, kb, m1, b, oflags, s);
   unsigned long long* uniq = (sorted == ka) ? kb : ka;
   {
     size_t tmp = 0;
@@ -393,6 +465,7 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   Scratch sc(s);
   int sms = sm_count();
   if (m > 0) {
+    TC_REQUIRE(((uintptr_t)edges & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
     int* bad = sc.alloc<int>(1);
     TC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
     k_range_check<<<grid_for(2 * m, kBlock, sms * 8), kBlock, 0, s>>>(edges, 2 * m, n, bad);
@@ -411,7 +484,7 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   int32_t* deg_orig = sc.alloc<int32_t>(n);
   TC_CUDA(cudaMemsetAsync(deg_orig, 0, n * sizeof(int32_t), s));
   if (m) {
-    k_histogram<<<grid_for(2 * m, kBlock, sms * 16), kBlock, 0, s>>>(edges, 2 * m, deg_orig);
+    k_histogram<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, deg_orig);
     check_launch();
   }
   // canonical order: ascending (degree, id) via a stable radix sort (graph.py:152)
@@ -437,7 +510,7 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   auto* ka = sc.alloc<unsigned long long>(m);
   auto* kb = sc.alloc<unsigned long long>(m);
   if (m) {
-    k_pack_pairs<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, b, ka);
+    k_pack_pairs<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, b, ka, nullptr);
     check_launch();
   }
   unsigned long long* keys = sort_keys(sc, ka, kb, m, 2 * b, s);

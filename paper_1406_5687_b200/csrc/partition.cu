@@ -238,8 +238,20 @@ __global__ void k_rec_emit(const int64_t* __restrict__ indptr, const int32_t* __
   }
 }
 
-__global__ void k_dest_counts(const uint32_t* __restrict__ dest, int64_t nrec, unsigned long long* counts) {
-  GRID_STRIDE(i, nrec) atomicAdd(&counts[dest[i]], 1ull);
+// records are sorted by destination: count per dest by binary search
+__global__ void k_dest_counts(const uint32_t* __restrict__ dest, int64_t nrec, int P, long long* counts) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P; j += gridDim.x * blockDim.x) {
+    auto lb = [&](uint32_t x) {
+      int64_t lo = 0, hi = nrec;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (dest[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      return lo;
+    };
+    counts[j] = lb((uint32_t)j + 1) - lb((uint32_t)j);
+  }
 }
 
 __global__ void k_pack_len(const int64_t* __restrict__ indptr, const int32_t* __restrict__ rec_v,
@@ -265,33 +277,52 @@ __global__ void k_pack(const int64_t* __restrict__ indptr, const int32_t* __rest
 }
 
 // For list l (ids[off[l], off[l+1])) and each position k holding an owned
-// id u in [lo, hi): segment (pool_base + off[l] + k + 1, pool_base + off[l+1])
-// for owner u - lo.  Pass 1 counts, pass 2 writes at reserved slots.
-__global__ void k_owner_segs(const int64_t* __restrict__ off, const int32_t* __restrict__ ids,
-                             int64_t nl, int64_t lo, int64_t hi, int64_t pool_base,
-                             unsigned long long* counter, int64_t cap, int32_t* owner,
-                             int2* segs) {
-  int lane = threadIdx.x & 31;
-  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t l = warp; l < nl; l += nwarps) {
-    int64_t a = off[l], b = off[l + 1];
+// id u in [lo, hi) with a non-empty suffix: segment (pool_base + k + 1,
+// pool_base + off[l+1]) for owner u - lo.  Warp per list; pass 1 counts per
+// list, a scan gives every list its output offset, pass 2 writes in list
+// order (no global atomics).
+__device__ __forceinline__ bool owned_pos(const int32_t* __restrict__ ids, int64_t k, int64_t b, int64_t lo,
+                                          int64_t hi, int32_t* u) {
+  if (k >= b) return false;
+  *u = ids[k];
+  return *u >= lo && *u < hi && k + 1 < b;  // empty suffixes carry no work
+}
+
+__global__ void k_owner_seg_count(const int64_t* __restrict__ off, const int32_t* __restrict__ ids, int64_t nl,
+                                  int64_t lo, int64_t hi, int64_t* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < nl; l += nwarps) {
+    const int64_t a = off[l], b = off[l + 1];
+    int c = 0;
     for (int64_t k = a + lane; k < b; k += 32) {
-      int64_t u = ids[k];
-      bool own = (u >= lo && u < hi) && (k + 1 < b);  // empty suffixes carry no work
-      unsigned m = __ballot_sync(__activemask(), own);
-      if (!m) continue;
-      unsigned long long base = 0;
-      int leader = __ffs(m) - 1;
-      if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
-      base = __shfl_sync(__activemask(), base, leader);
+      int32_t u;
+      c += owned_pos(ids, k, b, lo, hi, &u);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) cnt[l] = c;
+  }
+}
+
+__global__ void k_owner_seg_emit(const int64_t* __restrict__ off, const int32_t* __restrict__ ids, int64_t nl,
+                                 int64_t lo, int64_t hi, int64_t pool_base, const int64_t* __restrict__ out_off,
+                                 int32_t* owner, int2* segs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; l < nl; l += nwarps) {
+    const int64_t a = off[l], b = off[l + 1];
+    int64_t o = out_off[l];
+    for (int64_t k0 = a; k0 < b; k0 += 32) {
+      const int64_t k = k0 + lane;
+      int32_t u = 0;
+      const bool own = owned_pos(ids, k, b, lo, hi, &u);
+      const unsigned msk = __ballot_sync(0xffffffffu, own);
       if (own) {
-        int64_t slot = (int64_t)base + __popc(m & ((1u << lane) - 1));
-        if (owner && slot < cap) {
-          owner[slot] = (int32_t)(u - lo);
-          segs[slot] = make_int2((int)(pool_base + k + 1), (int)(pool_base + b));
-        }
+        const int64_t slot = o + __popc(msk & ((1u << lane) - 1u));
+        owner[slot] = u - (int32_t)lo;
+        segs[slot] = make_int2((int)(pool_base + k + 1), (int)(pool_base + b));
       }
+      o += __popc(msk);
     }
   }
 }
@@ -412,7 +443,7 @@ int tc_surrogate_records(const int64_t* eff_indptr, const int32_t* eff_indices, 
     }
     TC_CUDA(cudaMemcpyAsync(rec_v, vv, nrec * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     TC_CUDA(cudaMemcpyAsync(rec_dest, dk, nrec * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    tcb::k_dest_counts<<<tcb::grid_for(nrec, 256), 256, 0, s>>>(dk, nrec, reinterpret_cast<unsigned long long*>(counts));
+    tcb::k_dest_counts<<<tcb::grid_for(P, 128), 128, 0, s>>>(dk, nrec, P, counts);
     tcb::check_launch();
     tcb::sync_stream(s);
   });
@@ -447,22 +478,27 @@ int tc_owner_segments(const int64_t* list_offsets, const int32_t* list_ids, int6
                       int64_t* nseg_host, tc_stream_t stream) {
   return tcb::guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
-    tcb::Scratch sc(s);
-    auto* ctr = sc.alloc<unsigned long long>(1);
-    TC_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s));
     *nseg_host = 0;
     if (nl <= 0) return;
+    tcb::Scratch sc(s);
     int64_t last = 0;
     TC_CUDA(cudaMemcpyAsync(&last, list_offsets + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     tcb::sync_stream(s);
     TC_REQUIRE(pool_base >= 0 && pool_base + last < (1ll << 31), TC_EINVAL, "segment pool must stay below 2^31 ids");
-    tcb::k_owner_segs<<<tcb::grid_for(nl * 32, 256, tcb::sm_count() * 16), 256, 0, s>>>(
-        list_offsets, list_ids, nl, lo, hi, pool_base, ctr, cap, owner,
-        reinterpret_cast<int2*>(segs));
+    int64_t* cnt = sc.alloc<int64_t>(nl + 1);
+    int64_t* out_off = sc.alloc<int64_t>(nl + 1);
+    TC_CUDA(cudaMemsetAsync(cnt + nl, 0, sizeof(int64_t), s));
+    const int grid = tcb::grid_for(nl * 32, 256, tcb::sm_count() * 16);
+    tcb::k_owner_seg_count<<<grid, 256, 0, s>>>(list_offsets, list_ids, nl, lo, hi, cnt);
     tcb::check_launch();
-    unsigned long long c = tcb::read_scalar(ctr, s);
-    *nseg_host = (int64_t)c;
-    TC_REQUIRE(owner == nullptr || (int64_t)c <= cap, TC_EINVAL, "segment buffer too small");
+    tcb::exclusive_sum(sc, cnt, out_off, nl + 1, s);
+    const int64_t c = tcb::read_scalar(out_off + nl, s);
+    *nseg_host = c;
+    if (owner == nullptr || c == 0) return;
+    TC_REQUIRE(c <= cap, TC_EINVAL, "segment buffer too small");
+    tcb::k_owner_seg_emit<<<grid, 256, 0, s>>>(list_offsets, list_ids, nl, lo, hi, pool_base, out_off, owner,
+                                               reinterpret_cast<int2*>(segs));
+    tcb::check_launch();
   });
 }
 

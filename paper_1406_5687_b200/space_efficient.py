@@ -66,15 +66,13 @@ def owner_segments(list_offsets, list_ids, lo, hi, pool_base):
     """Device segments (owner, suffix) for owned ids found in the lists."""
     nl = int(list_offsets.numel()) - 1
     cnt = ctypes.c_int64()
-    _lib.call("tc_owner_segments", _lib.ptr(list_offsets), _lib.ptr(list_ids), nl, int(lo), int(hi),
-              int(pool_base), None, None, 0, ctypes.byref(cnt), _lib.stream())
-    k = cnt.value
+    cap = max(int(list_ids.numel()), 1)  # at most one segment per id
     dev = list_ids.device
-    owner = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
-    segs = torch.empty(max(2 * k, 2), dtype=torch.int32, device=dev)
+    owner = torch.empty(cap, dtype=torch.int32, device=dev)
+    segs = torch.empty(2 * cap, dtype=torch.int32, device=dev)
     _lib.call("tc_owner_segments", _lib.ptr(list_offsets), _lib.ptr(list_ids), nl, int(lo), int(hi),
-              int(pool_base), _lib.ptr(owner), _lib.ptr(segs), k, ctypes.byref(cnt), _lib.stream())
-    return owner, segs, k
+              int(pool_base), _lib.ptr(owner), _lib.ptr(segs), cap, ctypes.byref(cnt), _lib.stream())
+    return owner, segs, cnt.value
 
 
 def count_segments(tab_indptr, tab_indices, pool, owner, segs, nseg, n_owner, bounds=None):

@@ -1,0 +1,73 @@
+"""Per-rank step time of the multi-GPU surrogate / direct / replicated
+steps, emulated on one GPU (dev tool): each rank's device work runs in turn
+with the exchange replaced by local buffer passing, so max over ranks
+approximates the N-GPU step minus NCCL transfer time."""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1406_5687_b200 as tcb  # noqa: E402
+from paper_1406_5687_b200 import distributed as D  # noqa: E402
+from paper_1406_5687_b200.partitioning import balanced_bounds, partition_ranges, range_bounds  # noqa: E402
+from paper_1406_5687_b200.sequential import count_middle  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--ranks", default="2,4,8")
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+raw = bench.host_raw_edges(a.config, pin=True)
+g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw.cuda())))
+ops = D.DeviceOps()
+out = torch.empty(1, dtype=torch.int64, device="cuda")
+
+
+def timed(fn):
+    best = 1e9
+    for _ in range(a.reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
+t1 = timed(lambda: count_middle(g, out=out))
+print(f"{a.config}: 1 GPU count {t1:.3f} ms (wall, incl. host overhead)")
+for P in [int(x) for x in a.ranks.split(",")]:
+    sb = range_bounds(partition_ranges(g, tcb.CostKind.PRED_SUM, P))
+    shards = [D.shard_of(g, int(sb[r]), int(sb[r + 1])) for r in range(P)]
+    # surrogate: records+pack on the sender, segments+count on the receiver
+    send = [timed(lambda sh=sh, r=r: ops.pack(sh, ops.records(sh, sb, P, r)[0])) for r, sh in enumerate(shards)]
+    inbox = {r: [] for r in range(P)}
+    for r, sh in enumerate(shards):
+        rec_v, counts = ops.records(sh, sb, P, r)
+        lens, ids = ops.pack(sh, rec_v)
+        lens_np = lens.cpu().numpy()
+        s = i = 0
+        for j in range(P):
+            c = int(counts[j])
+            k = int(lens_np[s: s + c].sum())
+            if c:
+                inbox[j].append((lens[s: s + c], ids[i: i + k]))
+            s += c
+            i += k
+    recv = []
+    for r, sh in enumerate(shards):
+        rl = torch.cat([x[0] for x in inbox[r]]) if inbox[r] else torch.zeros(0, dtype=torch.int64, device="cuda")
+        ri = torch.cat([x[1] for x in inbox[r]]) if inbox[r] else torch.zeros(0, dtype=torch.int32, device="cuda")
+        recv.append(timed(lambda sh=sh, rl=rl, ri=ri: ops.count(sh, rl, ri)))
+    surr = [s + c for s, c in zip(send, recv)]
+    # replicated: middle engine over a cost-balanced u range
+    ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
+    ub = balanced_bounds(ucost, 0, g.n, P).cpu().numpy()
+    rep = [timed(lambda r=r: count_middle(g, int(ub[r]), int(ub[r + 1]), out=out)) for r in range(P)]
+    print(f"P={P}: surrogate max {max(surr):.3f} ms (send {max(send):.3f}, count {max(recv):.3f}) "
+          f"-> eff {t1 / (P * max(surr)):.2f}; replicated max {max(rep):.3f} ms -> eff {t1 / (P * max(rep)):.2f}")
