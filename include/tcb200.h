@@ -102,6 +102,20 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
                     int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, tc_stream_t stream);
 
+/* Reusable form of tc_count_middle for repeated counts of one graph: the
+ * plan (tier lists and chunk boundaries for owners [u0, u1)) is computed
+ * once (synchronises); tc_plan_run then only zeroes `out` and launches the
+ * engine (no host synchronisation, graph-capturable).  The plan keeps the
+ * argument pointers -- the caller keeps those arrays alive and unchanged --
+ * and re-plans itself if tc_set_tuning changed the tier caps. */
+typedef struct tc_plan_s* tc_plan_t;
+int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
+                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
+                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
+                   tc_stream_t stream);
+int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream);
+int tc_plan_free(tc_plan_t plan);
+
 /* Generic engine over k "virtual owners": owner x probes the table list
  * N^_{owner_map[x]} (owner_map NULL: identity) with segments
  * segs[row_indptr[x] .. row_indptr[x+1]) (int32 pairs into `pool`); cost_prefix

@@ -868,39 +868,75 @@ __global__ void k_tier_scatter(const int32_t* __restrict__ flag, const int32_t* 
   }
 }
 
-template <class Segs>
-void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* row_indptr, const int64_t* tab_indptr,
-                const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
-                const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
-                cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
-  (void)n_owner;
+// Device memory that outlives one call (engine plans): same interface as
+// Scratch, freed when the plan is destroyed.
+class Persist {
+ public:
+  Persist() = default;
+  Persist(const Persist&) = delete;
+  Persist& operator=(const Persist&) = delete;
+  ~Persist() { release(); }
+  void set_stream(cudaStream_t s) { s_ = s; }
+  void release() {
+    for (void* p : ptrs_) cudaFreeAsync(p, 0);
+    ptrs_.clear();
+  }
+  void* bytes(size_t n) {  // pool allocation, valid on every stream once s_ has synchronised
+    void* p = nullptr;
+    TC_CUDA(cudaMallocAsync(&p, n ? n : 16, s_));
+    ptrs_.push_back(p);
+    return p;
+  }
+  template <class T>
+  T* alloc(int64_t n) {
+    return static_cast<T*>(bytes(sizeof(T) * (size_t)(n > 0 ? n : 1)));
+  }
+
+ private:
+  std::vector<void*> ptrs_;
+  cudaStream_t s_ = 0;
+};
+
+// Everything one engine run needs beyond the graph: per tier the compacted
+// owner list, rows, chunk plan and queue counter (EngineArgs.out is set per
+// run).  Built by prepare_engine, consumed by launch_engine.
+struct EngineLaunch {
+  unsigned long long hsz[3] = {0, 0, 0};
+  EngineArgs args[3];
+  int* queue[3] = {nullptr, nullptr, nullptr};
+};
+
+template <class Segs, class Alloc>
+EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const int64_t* row_indptr,
+                            const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* pool, int64_t x0,
+                            int64_t x1, const int64_t* bucket_bounds, int nbuckets, Segs segs, cudaStream_t s,
+                            const int32_t* owner_map = nullptr, int mode = 0) {
   const TierShape& ts = tier_shape();
   const int64_t nx = x1 - x0;
   const int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
   const int grid = grid_for(nx + 1, 256, sm_count() * 16);
+  EngineLaunch L;
   int32_t* flag[3];
-  for (int k = 0; k < 3; ++k) flag[k] = sc.alloc<int32_t>(nx + 1);
-  auto* sizes = sc.alloc<unsigned long long>(3);
+  for (int k = 0; k < 3; ++k) flag[k] = tmp_sc.alloc<int32_t>(nx + 1);
+  auto* sizes = tmp_sc.alloc<unsigned long long>(3);
   TC_CUDA(cudaMemsetAsync(sizes, 0, 3 * sizeof(unsigned long long), s));
   k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2], sizes);
   check_launch();
-  unsigned long long hsz[3];
-  TC_CUDA(cudaMemcpyAsync(hsz, sizes, sizeof(hsz), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaMemcpyAsync(L.hsz, sizes, sizeof(L.hsz), cudaMemcpyDeviceToHost, s));
   sync_stream(s);  // empty tiers are skipped entirely
   size_t tmp = 0, tmp2 = 0;
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag[0], flag[0], nx + 1, s));
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (int64_t*)nullptr, (int64_t*)nullptr, nx + 1, s));
-  void* t = sc.bytes(std::max(tmp, tmp2));
-  EngineArgs args[3];
+  void* t = tmp_sc.bytes(std::max(tmp, tmp2));
   for (int k = 0; k < 3; ++k) {
-    if (hsz[k] == 0) continue;
-    int32_t* pos = sc.alloc<int32_t>(nx + 1);
+    if (L.hsz[k] == 0) continue;
+    int32_t* pos = tmp_sc.alloc<int32_t>(nx + 1);
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, flag[k], pos, nx + 1, s));
-    int32_t* own = sc.alloc<int32_t>(nx + 1);
-    int64_t* len = sc.alloc<int64_t>(nx + 1);
-    int64_t* cst = sc.alloc<int64_t>(nx + 1);
-    int64_t* vrow = sc.alloc<int64_t>(nx + 1);
-    int64_t* vcost = sc.alloc<int64_t>(nx + 1);
+    int32_t* own = al.template alloc<int32_t>(nx + 1);
+    int64_t* len = tmp_sc.alloc<int64_t>(nx + 1);
+    int64_t* cst = tmp_sc.alloc<int64_t>(nx + 1);
+    int64_t* vrow = al.template alloc<int64_t>(nx + 1);
+    int64_t* vcost = tmp_sc.alloc<int64_t>(nx + 1);
     TC_CUDA(cudaMemsetAsync(len, 0, (nx + 1) * sizeof(int64_t), s));
     TC_CUDA(cudaMemsetAsync(cst, 0, (nx + 1) * sizeof(int64_t), s));
     k_tier_scatter<<<grid, 256, 0, s>>>(flag[k], pos, x0, nx, row_indptr, cp, own, len, cst);
@@ -908,23 +944,23 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, len, vrow, nx + 1, s));
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, cst, vcost, nx + 1, s));
     const int nmax = 10 * ts.workers[k] + 8;
-    int64_t* chunk_r = sc.alloc<int64_t>(nmax + 1);
-    int32_t* chunk_x = sc.alloc<int32_t>(nmax);
-    int* ctl = sc.alloc<int>(2);  // [0] nchunks, [1] queue
+    int64_t* chunk_r = al.template alloc<int64_t>(nmax + 1);
+    int32_t* chunk_x = al.template alloc<int32_t>(nmax);
+    int* ctl = al.template alloc<int>(2);  // [0] nchunks, [1] queue
     TC_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), s));
     if (k == 2) {  // block tier: hub segments vary wildly in cost -> plan on an exact per-segment prefix
       int64_t nseg = 0;
       TC_CUDA(cudaMemcpyAsync(&nseg, vrow + nx, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       sync_stream(s);
-      int64_t* scost = sc.alloc<int64_t>(nseg + 1);
-      int64_t* sp = sc.alloc<int64_t>(nseg + 1);
+      int64_t* scost = tmp_sc.alloc<int64_t>(nseg + 1);
+      int64_t* sp = tmp_sc.alloc<int64_t>(nseg + 1);
       TC_CUDA(cudaMemsetAsync(scost + nseg, 0, sizeof(int64_t), s));
-      k_seg_cost<<<grid_for((int64_t)hsz[k] * 32, 256, sm_count() * 16), 256, 0, s>>>(
-          own, vrow, row_indptr, owner_map, tab_indptr, (int64_t)hsz[k], segs, scost);
+      k_seg_cost<<<grid_for((int64_t)L.hsz[k] * 32, 256, sm_count() * 16), 256, 0, s>>>(
+          own, vrow, row_indptr, owner_map, tab_indptr, (int64_t)L.hsz[k], segs, scost);
       check_launch();
       size_t tmp3 = 0;
       TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp3, scost, sp, nseg + 1, s));
-      void* t3 = sc.bytes(tmp3);
+      void* t3 = tmp_sc.bytes(tmp3);
       TC_CUDA(cub::DeviceScan::ExclusiveSum(t3, tmp3, scost, sp, nseg + 1, s));
       k_plan_seg<<<grid_for(nmax + 1, 256), 256, 0, s>>>(sp, nseg, vrow, nx, ts.workers[k], nmax, chunk_r, chunk_x,
                                                          ctl);
@@ -935,8 +971,21 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
     check_launch();
     const int64_t lo = k == 0 ? 0 : (k == 1 ? c0 : c1);
     const int64_t hi = k == 0 ? c0 : (k == 1 ? c1 : INT64_MAX);
-    args[k] = EngineArgs{vrow, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
-                         bucket_bounds, nbuckets, out, nx, owner_map, lo, hi, g_big_cap, own, row_indptr};
+    L.args[k] = EngineArgs{vrow, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
+                           bucket_bounds, nbuckets, nullptr, nx, owner_map, lo, hi, g_big_cap, own, row_indptr};
+    L.queue[k] = ctl + 1;
+  }
+  return L;
+}
+
+// Launches the non-empty tiers (queue counters reset first); `out` must be
+// zeroed by the caller.
+template <class Segs>
+void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStream_t s) {
+  const TierShape& ts = tier_shape();
+  for (int k = 0; k < 3; ++k) {
+    L.args[k].out = out;
+    if (L.hsz[k]) TC_CUDA(cudaMemsetAsync(L.queue[k], 0, sizeof(int), s));
   }
   if (g_time_engine) {
     if (!g_ev[0]) {
@@ -948,18 +997,18 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
       for (auto& e : g_tev) TC_CUDA(cudaEventCreate(&e));
     TC_CUDA(cudaEventRecord(g_tev[0], s));
   }
-  if (hsz[0]) {
-    K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(args[0], segs);
+  if (L.hsz[0]) {
+    K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
     check_launch();
   }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[1], s));
-  if (hsz[1]) {
-    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(args[1], segs);
+  if (L.hsz[1]) {
+    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
     check_launch();
   }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[2], s));
-  if (hsz[2]) {
-    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(args[2], segs);
+  if (L.hsz[2]) {
+    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
     check_launch();
   }
   if (g_time_engine) {
@@ -975,6 +1024,46 @@ void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* 
     }
     ++g_engine_launches;
   }
+}
+
+template <class Segs>
+void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* row_indptr, const int64_t* tab_indptr,
+                const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
+                const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
+                cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
+  (void)n_owner;
+  EngineLaunch L = prepare_engine(sc, sc, cp, row_indptr, tab_indptr, tab_indices, pool, x0, x1, bucket_bounds,
+                                  nbuckets, segs, s, owner_map, mode);
+  launch_engine(L, out, segs, s);
+}
+
+// A reusable middle-vertex engine run over a fixed (graph, owner range):
+// the tier lists and chunk plan are computed once; every run is the memsets
+// plus the engine launches, with no host synchronisation.  The plan keeps
+// the caller's array pointers and re-plans itself if the tier caps changed.
+struct MiddlePlan {
+  const int64_t *tab_indptr, *rev_indptr, *rev_cost, *bucket_bounds;
+  const int32_t *tab_indices, *rev_seg, *pool;
+  int64_t n, u0, u1;
+  int nbuckets;
+  int caps[3];
+  Persist mem;
+  EngineLaunch L;
+};
+
+static void plan_build(MiddlePlan& P, cudaStream_t s) {
+  P.mem.release();
+  P.mem.set_stream(s);
+  P.L = EngineLaunch{};
+  P.caps[0] = g_warp_cap;
+  P.caps[1] = g_mid_cap;
+  P.caps[2] = g_big_cap;
+  if (P.u1 <= P.u0) return;
+  Scratch sc(s);
+  P.L = prepare_engine(P.mem, sc, P.rev_cost, P.rev_indptr, P.tab_indptr, P.tab_indices, P.pool, P.u0, P.u1,
+                       P.bucket_bounds, P.nbuckets, PullSegs{reinterpret_cast<const int2*>(P.rev_seg)}, s,
+                       nullptr, 1);
+  sync_stream(s);
 }
 
 void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
@@ -1085,6 +1174,46 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
     tcb::count_middle(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, n, u0, u1,
                       bucket_bounds, nbuckets, out, (cudaStream_t)stream);
   });
+}
+
+int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
+                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
+                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
+                   tc_stream_t stream) {
+  return tcb::guarded([&] {
+    TC_REQUIRE(plan != nullptr, TC_EINVAL, "plan out-pointer is NULL");
+    *plan = nullptr;
+    TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
+    TC_REQUIRE(nbuckets >= 1, TC_EINVAL, "nbuckets must be >= 1");
+    TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
+    TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned");
+    auto* P = new tcb::MiddlePlan{tab_indptr, rev_indptr, rev_cost, bucket_bounds, tab_indices, rev_seg, pool,
+                                  n, u0, u1, nbuckets, {0, 0, 0}, {}, {}};
+    try {
+      tcb::plan_build(*P, (cudaStream_t)stream);
+    } catch (...) {
+      delete P;
+      throw;
+    }
+    *plan = reinterpret_cast<tc_plan_t>(P);
+  });
+}
+
+int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    TC_REQUIRE(plan != nullptr, TC_EINVAL, "NULL plan");
+    auto* P = reinterpret_cast<tcb::MiddlePlan*>(plan);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (P->caps[0] != tcb::g_warp_cap || P->caps[1] != tcb::g_mid_cap || P->caps[2] != tcb::g_big_cap)
+      tcb::plan_build(*P, s);
+    TC_CUDA(cudaMemsetAsync(out, 0, P->nbuckets * sizeof(unsigned long long), s));
+    if (P->u1 <= P->u0) return;
+    tcb::launch_engine(P->L, out, tcb::PullSegs{reinterpret_cast<const int2*>(P->rev_seg)}, s);
+  });
+}
+
+int tc_plan_free(tc_plan_t plan) {
+  return tcb::guarded([&] { delete reinterpret_cast<tcb::MiddlePlan*>(plan); });
 }
 
 int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,

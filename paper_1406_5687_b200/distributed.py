@@ -31,7 +31,7 @@ check the protocol with gloo at world_size 2.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -48,6 +48,9 @@ class Shard:
     hi: int
     indptr: torch.Tensor   # int64[hi - lo + 1], local offsets (indptr[0] == 0)
     indices: torch.Tensor  # int32[m_local (+4 padding)], global canonical ids
+    # derived from the shard's own lists only, built on first use (the pull
+    # index of count_direct: local segments grouped by owner)
+    cache: dict = field(default_factory=dict, repr=False, compare=False)
 
     @property
     def m(self):
@@ -155,11 +158,16 @@ class DeviceOps:
 
     def count_direct(self, shard: Shard, req_ids, fetched_len, fetched_ids):
         """Direct scheme, step 4: count_node_range(lo, hi) over the shard's
-        lists and the fetched N^_u (lowest-vertex attribution)."""
+        lists and the fetched N^_u (lowest-vertex attribution), with the
+        middle-vertex engine: tables N^_u from the lookup CSR (own rows +
+        fetched rows), segments = suffixes of the shard's own lists only,
+        grouped by owner once per shard (Shard.cache)."""
+        from .space_efficient import owner_segments, segments_csr
+
         L = self._lib
         dev = shard.indptr.device
         nloc = shard.hi - shard.lo
-        if nloc == 0:
+        if nloc == 0 or shard.m == 0:
             return 0
         nreq = int(req_ids.numel())
         n_rows = max(shard.hi, int(req_ids[-1].item()) + 1 if nreq else 0)
@@ -171,9 +179,17 @@ class DeviceOps:
         pool = torch.zeros(ml + mr + 4, dtype=torch.int32, device=dev)  # +4: 16-byte chunk reads
         pool[:ml] = shard.indices[:ml]
         pool[ml: ml + mr] = fetched_ids
+        key = ("pull", n_rows)
+        idx = shard.cache.get(key)
+        if idx is None:
+            owner, segs, k = owner_segments(shard.indptr, pool[:ml], 0, n_rows, 0)
+            idx = segments_csr(owner[:k].contiguous(), segs[: 2 * k].contiguous(), k, n_rows, indptr)
+            shard.cache.clear()
+            shard.cache[key] = idx
+        row, rsegs, cost = idx
         out = torch.empty(1, dtype=torch.int64, device=dev)
-        L.call("tc_count_lowest", L.ptr(indptr), L.ptr(pool), n_rows, shard.lo, shard.hi, None, 1, L.ptr(out),
-               L.stream())
+        L.call("tc_count_middle", L.ptr(indptr), L.ptr(pool), L.ptr(row), L.ptr(rsegs), L.ptr(cost), L.ptr(pool),
+               n_rows, 0, n_rows, None, 1, L.ptr(out), L.stream())
         return int(out.item())
 
 def _a2a_counts(counts_np, group, device):

@@ -38,6 +38,32 @@ def intersect_count(a, b) -> int:
     return int(out.item())
 
 
+class _MiddlePlan:
+    """Owner of a tc_plan_t (tier lists + chunk plan of one (graph, range)),
+    cached on the Graph; freed with it."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self, g: Graph, u0: int, u1: int):
+        import ctypes
+
+        h = ctypes.c_void_p()
+        _lib.call("tc_plan_middle", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(g._rev_indptr),
+                  _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost), _lib.ptr(g.eff_indices), g.n, u0, u1, None, 1,
+                  ctypes.byref(h), _lib.stream())
+        self.handle = h
+
+    def run(self, out):
+        _lib.call("tc_plan_run", self.handle, _lib.ptr(out), _lib.stream())
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.lib().tc_plan_free(self.handle)
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
 def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
     """Middle-vertex engine over u in [u0, u1), optionally binned by `bounds`
     (device int64[k+1]).  Returns the device uint64 counts (as int64).
@@ -57,6 +83,13 @@ def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
         _lib.call("tc_count_owners", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(t.owner_u),
                   _lib.ptr(t.owner_ptr), _lib.ptr(t.segs), _lib.ptr(t.cost), _lib.ptr(g.eff_indices), t.k,
                   _lib.ptr(bounds), k, _lib.ptr(out), 1, _lib.stream())
+        return out
+    if bounds is None:  # repeated counts of one graph reuse the engine plan
+        key = ("middle_plan", int(u0), int(u1))
+        plan = g._cache.get(key)
+        if plan is None:
+            plan = g._cache[key] = _MiddlePlan(g, int(u0), int(u1))
+        plan.run(out)
         return out
     _lib.call("tc_count_middle", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices),
               _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost),

@@ -75,15 +75,23 @@ def owner_segments(list_offsets, list_ids, lo, hi, pool_base):
     return owner, segs, cnt.value
 
 
-def count_segments(tab_indptr, tab_indices, pool, owner, segs, nseg, n_owner, bounds=None):
-    """Middle-vertex engine over explicit segments (tables indexed 0..n_owner)."""
-    dev = pool.device
+def segments_csr(owner, segs, nseg, n_owner, tab_indptr):
+    """Segments grouped by owner: (row_indptr, row_segs, cost_prefix) for the
+    middle-vertex engine (tables tab_indptr indexed 0..n_owner)."""
+    dev = segs.device
     row = torch.empty(n_owner + 1, dtype=torch.int64, device=dev)
     rsegs = torch.empty(max(2 * nseg, 2), dtype=torch.int32, device=dev)
     cost = torch.empty(n_owner + 1, dtype=torch.int64, device=dev)
-    tab_indptr = tab_indptr.contiguous()
     _lib.call("tc_segments_csr", _lib.ptr(owner), _lib.ptr(segs), int(nseg), int(n_owner),
-              _lib.ptr(tab_indptr), _lib.ptr(row), _lib.ptr(rsegs), _lib.ptr(cost), _lib.stream())
+              _lib.ptr(tab_indptr.contiguous()), _lib.ptr(row), _lib.ptr(rsegs), _lib.ptr(cost), _lib.stream())
+    return row, rsegs, cost
+
+
+def count_segments(tab_indptr, tab_indices, pool, owner, segs, nseg, n_owner, bounds=None):
+    """Middle-vertex engine over explicit segments (tables indexed 0..n_owner)."""
+    dev = pool.device
+    tab_indptr = tab_indptr.contiguous()
+    row, rsegs, cost = segments_csr(owner, segs, nseg, n_owner, tab_indptr)
     k = 1 if bounds is None else int(bounds.numel()) - 1
     out = torch.empty(k, dtype=torch.int64, device=dev)
     _lib.call("tc_count_middle", _lib.ptr(tab_indptr), _lib.ptr(tab_indices), _lib.ptr(row),

@@ -65,6 +65,34 @@ for P in [int(x) for x in a.ranks.split(",")]:
         ri = torch.cat([x[1] for x in inbox[r]]) if inbox[r] else torch.zeros(0, dtype=torch.int32, device="cuda")
         recv.append(timed(lambda sh=sh, rl=rl, ri=ri: ops.count(sh, rl, ri)))
     surr = [s + c for s, c in zip(send, recv)]
+    # direct pull (deduplicated requests, lowest-vertex partials via the
+    # middle engine over the shard's cached pull index)
+    for cname, ck in (("predsum", tcb.CostKind.PRED_SUM), ("succsum", tcb.CostKind.SUCC_SUM)):
+        db = range_bounds(partition_ranges(g, ck, P))
+        dsh = [D.shard_of(g, int(db[r]), int(db[r + 1])) for r in range(P)]
+        asks = [ops.requests(sh, db, P, r) for r, sh in enumerate(dsh)]
+        t_req = [timed(lambda sh=sh, r=r: ops.requests(sh, db, P, r)) for r, sh in enumerate(dsh)]
+        serve = [0.0] * P
+        fetched = []
+        for i in range(P):
+            ids_i, _, counts_i, _ = asks[i]
+            parts = []
+            a0 = 0
+            for j in range(P):
+                c = int(counts_i[j])
+                if c:
+                    q = ids_i[a0: a0 + c]
+                    serve[j] += timed(lambda sh=dsh[j], q=q: ops.pack(sh, q))
+                    parts.append(ops.pack(dsh[j], q))
+                a0 += c
+            fl = torch.cat([p_[0] for p_ in parts]) if parts else torch.zeros(0, dtype=torch.int64, device="cuda")
+            fi = torch.cat([p_[1] for p_ in parts]) if parts else torch.zeros(0, dtype=torch.int32, device="cuda")
+            fetched.append((fl, fi))
+        cnt = [timed(lambda r=r: ops.count_direct(dsh[r], asks[r][0], *fetched[r])) for r in range(P)]
+        tot = [t_req[r] + serve[r] + cnt[r] for r in range(P)]
+        words = sum(int(f[1].numel()) for f in fetched)
+        print(f"P={P}: direct-pull[{cname}] max {max(tot):.3f} ms (req {max(t_req):.3f}, serve {max(serve):.3f}, "
+              f"count {max(cnt):.3f}; fetched {words / 1e6:.1f}M ids) -> eff {t1 / (P * max(tot)):.2f}")
     # replicated: middle engine over a cost-balanced u range
     ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
     ub = balanced_bounds(ucost, 0, g.n, P).cpu().numpy()
