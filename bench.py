@@ -17,6 +17,9 @@ N > 1 (torchrun, one rank per GPU): every rank builds the graph, owns a
 contiguous middle-vertex range balanced by the engine's cost prefix and the
 per-GPU uint64 counts are combined with an NCCL all-reduce inside the timed
 region; timing is the max over ranks ("strong" scaling: total work fixed).
+--mode surrogate / direct run the paper's space-efficient schemes instead
+(node-range shards, N^ lists exchanged with NCCL all-to-all, then the
+all-reduce; distributed.py).
 """
 
 from __future__ import annotations
@@ -244,8 +247,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
-    ap.add_argument("--mode", default="surrogate", choices=["surrogate", "replicated"],
-                    help="N>1: the paper's non-overlapping partition with list exchange, or replicated graph")
+    ap.add_argument("--mode", default="replicated", choices=["replicated", "surrogate", "direct"],
+                    help="N>1: replicated graph with cost-balanced middle-vertex ranges (default), the paper's "
+                         "non-overlapping partition with surrogate list exchange, or the direct scheme as a "
+                         "deduplicated pull")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: --warmup < 3 is below the timing contract; using 3")
@@ -313,16 +318,20 @@ def _gpu_arm_core(args):
     else:
         u0, u1 = 0, n
     out = torch.empty(1, dtype=torch.int64, device=dev)
-    if mode == "surrogate":
-        from paper_1406_5687_b200.distributed import shard_of, surrogate_rank
+    if mode in ("surrogate", "direct"):
+        from paper_1406_5687_b200.distributed import direct_rank, shard_of, surrogate_rank
         from paper_1406_5687_b200.partitioning import partition_ranges, range_bounds
 
-        sb = range_bounds(partition_ranges(g, tcb.CostKind.PRED_SUM, world))
+        # surrogate: the reference's PRED_SUM ranges; direct: SUCC_SUM, the
+        # lowest-vertex work each rank's own lists generate
+        kind = tcb.CostKind.PRED_SUM if mode == "surrogate" else tcb.CostKind.SUCC_SUM
+        sb = range_bounds(partition_ranges(g, kind, world))
         shard = shard_of(g, int(sb[rank]), int(sb[rank + 1]))
+        rank_fn = surrogate_rank if mode == "surrogate" else direct_rank
 
     def count_step():
-        if mode == "surrogate":
-            total, _ = surrogate_rank(shard, sb)
+        if mode in ("surrogate", "direct"):
+            total, _ = rank_fn(shard, sb)
             out.fill_(total)
             return out
         count_middle(g, u0, u1, out=out)
@@ -367,7 +376,7 @@ def _gpu_arm_core(args):
 
     e2e_ms = None
     if not args.no_e2e:
-        if mode == "surrogate":
+        if mode in ("surrogate", "direct"):
             del shard
         del g
         torch.cuda.empty_cache()
@@ -378,8 +387,8 @@ def _gpu_arm_core(args):
             s.record()
             dev_raw = raw_host.to(dev, non_blocking=True)
             gg = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=dev_raw)))
-            if mode == "surrogate":
-                tri, _ = surrogate_rank(shard_of(gg, int(sb[rank]), int(sb[rank + 1])), sb)
+            if mode in ("surrogate", "direct"):
+                tri, _ = rank_fn(shard_of(gg, int(sb[rank]), int(sb[rank + 1])), sb)
             elif world > 1:
                 c = count_middle(gg, u0, u1)
                 dist.all_reduce(c)
@@ -422,11 +431,13 @@ def _gpu_arm_core(args):
         "data": "synthetic (seeded generator; no dataset)",
         "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw,
                    "triangles": T, "W_succsum": W,
-                   "l2": "inputs > L2 (rev_seg 16 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
+                   "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
                    "parallelism": {"single": "1 GPU",
                                    "replicated": f"{world} GPUs, replicated graph, cost-balanced middle-vertex ranges + NCCL all-reduce",
                                    "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
-                                                "(NCCL all-to-all) + NCCL all-reduce"}[mode]},
+                                                "(NCCL all-to-all) + NCCL all-reduce",
+                                   "direct": f"{world} GPUs, SUCC_SUM node-range shards, deduplicated pull of remote "
+                                             "N^_u (NCCL all-to-all) + NCCL all-reduce"}[mode]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_engine<PullSegs> (middle-vertex engine)",

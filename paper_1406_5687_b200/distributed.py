@@ -106,8 +106,30 @@ class DeviceOps:
                L.stream())
         return offs[1:] - offs[:-1], ids[: tot.value]
 
+    def _local_plan(self, shard: Shard):
+        """Engine plan over the shard's own lists (owned u, local
+        predecessors), built once per shard: the part of step 4 that does
+        not depend on what was received."""
+        from .space_efficient import owner_segments, segments_csr
+
+        L = self._lib
+        plan = shard.cache.get("surrogate_local")
+        if plan is None:
+            nloc, ml = shard.hi - shard.lo, shard.m
+            pool = torch.zeros(ml + 4, dtype=torch.int32, device=shard.indptr.device)  # aligned + padded
+            pool[:ml] = shard.indices[:ml]
+            owner, segs, k = owner_segments(shard.indptr, pool[: max(ml, 1)], shard.lo, shard.hi, 0)
+            row, rsegs, cost = segments_csr(owner[:k].contiguous(), segs[: 2 * k].contiguous(), k, nloc,
+                                            shard.indptr)
+            h = ctypes.c_void_p()
+            L.call("tc_plan_middle", L.ptr(shard.indptr), L.ptr(pool), L.ptr(row), L.ptr(rsegs), L.ptr(cost),
+                   L.ptr(pool), nloc, 0, nloc, None, 1, ctypes.byref(h), L.stream())
+            plan = shard.cache["surrogate_local"] = _PlanHandle(h, (pool, row, rsegs, cost))
+        return plan
+
     def count(self, shard: Shard, recv_len, recv_ids, bounds=None):
-        """Triangles with middle vertex in the shard's range (step 4)."""
+        """Triangles with middle vertex in the shard's range (step 4): the
+        cached local plan plus one engine run over the received lists."""
         from .space_efficient import count_segments, owner_segments
 
         L = self._lib
@@ -115,29 +137,20 @@ class DeviceOps:
         nloc = shard.hi - shard.lo
         if nloc == 0:
             return 0
-        # pool = local ids ++ received ids (16-byte aligned, padded)
-        ml, mr = shard.m, int(recv_ids.numel())
-        base_r = (ml + 3) // 4 * 4
-        pool = torch.zeros(base_r + mr + 4, dtype=torch.int32, device=dev)
-        pool[:ml] = shard.indices[:ml]
-        pool[base_r: base_r + mr] = recv_ids
-        owners, segs = [], []
-        o1, s1, k1 = owner_segments(shard.indptr, pool[:ml] if ml else pool[:1], shard.lo, shard.hi, 0)
-        if k1:
-            owners.append(o1[:k1])
-            segs.append(s1[: 2 * k1])
-        if recv_len.numel():
+        out = torch.empty(2, dtype=torch.int64, device=dev)
+        out[1:].zero_()
+        L.call("tc_plan_run", self._local_plan(shard).handle, L.ptr(out), L.stream())
+        mr = int(recv_ids.numel())
+        if recv_len.numel() and mr:
+            pool = torch.zeros(mr + 4, dtype=torch.int32, device=dev)  # aligned + padded
+            pool[:mr] = recv_ids
             roffs = torch.zeros(recv_len.numel() + 1, dtype=torch.int64, device=dev)
             roffs[1:] = torch.cumsum(recv_len.to(dev), 0)
-            o2, s2, k2 = owner_segments(roffs, recv_ids if mr else pool[:1], shard.lo, shard.hi, base_r)
+            o2, s2, k2 = owner_segments(roffs, pool[:mr], shard.lo, shard.hi, 0)
             if k2:
-                owners.append(o2[:k2])
-                segs.append(s2[: 2 * k2])
-        if not owners:
-            return 0
-        owner = torch.cat(owners).contiguous()
-        seg = torch.cat(segs).contiguous()
-        return int(count_segments(shard.indptr, shard.indices, pool, owner, seg, int(owner.numel()), nloc))
+                out[1] = count_segments(shard.indptr, shard.indices, pool, o2[:k2].contiguous(),
+                                        s2[: 2 * k2].contiguous(), k2, nloc)
+        return int(out.sum().item())
 
     def requests(self, shard: Shard, bounds, P, rank):
         """Direct scheme, step 1: (req_ids int32 ascending, req_mult int64,
@@ -191,6 +204,23 @@ class DeviceOps:
         L.call("tc_count_middle", L.ptr(indptr), L.ptr(pool), L.ptr(row), L.ptr(rsegs), L.ptr(cost), L.ptr(pool),
                n_rows, 0, n_rows, None, 1, L.ptr(out), L.stream())
         return int(out.item())
+
+class _PlanHandle:
+    """A tc_plan_t plus the device arrays it points into."""
+
+    __slots__ = ("handle", "keep")
+
+    def __init__(self, handle, keep):
+        self.handle, self.keep = handle, keep
+
+    def __del__(self):
+        try:
+            if self.handle:
+                from . import _lib
+                _lib.lib().tc_plan_free(self.handle)
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
 
 def _a2a_counts(counts_np, group, device):
     """all_to_all of one int64 per peer (step 2)."""
