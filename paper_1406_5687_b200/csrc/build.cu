@@ -233,17 +233,22 @@ __global__ void k_degrees(const int64_t* __restrict__ indptr, const int32_t* __r
 
 // Reverse CSR by counting scatter: edge i = (v, u) of the forward list
 // (keys sorted by (v, u)) goes to a slot of row u claimed with an atomic
-// cursor.  Row order is therefore unspecified -- the pull engine only sums
-// over a row -- and the full CSR sorts its rows when it is assembled.
+// cursor -- non-empty suffixes from the front of the row, empty ones (u is
+// the last id of N^_v) from the back, so the engine's segment groups are
+// prefix-dense and need no compaction.  Order within those two parts is
+// unspecified (the pull engine only sums over a row); the full CSR sorts
+// its rows when it is assembled.
 __global__ void k_rev_scatter(const unsigned long long* __restrict__ keys, int64_t m, int b,
                               const int64_t* __restrict__ eff_indptr, const int64_t* __restrict__ rev_indptr,
-                              int32_t* cursor, int2* rev_seg) {
+                              int32_t* cursor, int32_t* back, int2* rev_seg) {
   const unsigned long long mask = (1ull << b) - 1;
   GRID_STRIDE(i, m) {
     const unsigned long long k = keys[i];
     const int64_t v = (int64_t)(k >> b), u = (int64_t)(k & mask);
-    const int64_t slot = rev_indptr[u] + atomicAdd(&cursor[u], 1);
-    rev_seg[slot] = make_int2((int)(i + 1), (int)eff_indptr[v + 1]);
+    const int64_t end = eff_indptr[v + 1];
+    const int64_t slot = (i + 1 < end) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
+                                       : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
+    rev_seg[slot] = make_int2((int)(i + 1), (int)end);
   }
 }
 
@@ -532,10 +537,10 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in_deg, rev_indptr, n + 1, s));
   }
   if (m) {
-    int32_t* cursor = sc.alloc<int32_t>(n);
-    TC_CUDA(cudaMemsetAsync(cursor, 0, n * sizeof(int32_t), s));
+    int32_t* cursor = sc.alloc<int32_t>(2 * n);
+    TC_CUDA(cudaMemsetAsync(cursor, 0, 2 * n * sizeof(int32_t), s));
     k_rev_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indptr, rev_indptr, cursor,
-                                                                   reinterpret_cast<int2*>(rev_seg));
+                                                                   cursor + n, reinterpret_cast<int2*>(rev_seg));
     check_launch();
   }
   // pull-engine cost prefix over u

@@ -320,7 +320,11 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   int len = (int)(e - s);
   unsigned nz = __ballot_sync(FULL, len > 0);  // compact non-empty segments to the low lanes
   int nseg = __popc(nz);
-  int src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
+  // rows keep non-empty segments first (build.cu k_rev_scatter; owner
+  // segments never emit empty ones), so nz is almost always a low-lane
+  // prefix and the compaction is the identity
+  int src = lane;
+  if (nz & (nz + 1u)) src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
   int64_t cs = __shfl_sync(FULL, s, src);
   int clen = __shfl_sync(FULL, len, src);
   if (lane >= nseg) clen = 0;
