@@ -65,7 +65,7 @@ static constexpr int kLbBig = 11;         // block tier buckets: 2^11 x 4 ids (3
 static constexpr int kPosCap = 512;       // block tier: per-warp queue of filter hits
 static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
 static constexpr size_t kBigSmem = (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
-                                   sizeof(int32_t) * kPosCap * kBigWarps;
+                                   sizeof(int32_t) * kPosCap * kBigWarps + sizeof(int4) * 32 * kBigWarps;
 static constexpr int kSegCost = 2;        // must match build.cu
 static constexpr int kTabCost = 16;
 static constexpr int32_t kEmpty = -1;
@@ -273,8 +273,8 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 // count << 2).
 template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
-                                            int endx, int edge, int64_t delta, int total, int lane,
-                                            int& npos, uint32_t& cnt) {
+                                            const int4* __restrict__ segtab, int total, int lane, int& npos,
+                                            uint32_t& cnt) {
   const unsigned FULL = 0xffffffffu;
   const bool lane_seg = lane < nseg;
   for (int base = 0; base < total; base += 32 * kW) {
@@ -291,12 +291,11 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
         unsigned bit = (lane_seg && excl > b && excl < b + 32) ? (1u << (excl - b)) : 0u;
         unsigned starts = __reduce_or_sync(FULL, bit);
         int sj = c0 + __popc(starts & ((2u << lane) - 1u));
-        int64_t dl = __shfl_sync(FULL, delta, sj);
-        int ex = __shfl_sync(FULL, excl, sj);
-        int en = __shfl_sync(FULL, endx, sj);
-        int eg = __shfl_sync(FULL, edge, sj);
         int f = b + lane;
         if (f < total) {
+          const int4 q = segtab[sj];  // (delta lo, delta hi, excl, endx << 5 | edge)
+          const int64_t dl = (int64_t)(((uint64_t)(uint32_t)q.y << 32) | (uint32_t)q.x);
+          const int ex = q.z, en = q.w >> 5, eg = q.w & 31;
           v[k] = __ldg(&pool4[dl + f]);
           uint32_t lo = (f == ex) ? (uint32_t)(eg & 3) : 0u;
           uint32_t hi = (f == en - 1) ? (uint32_t)(eg >> 2) : 4u;
@@ -310,10 +309,12 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
   }
 }
 
-// One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner.
+// One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner;
+// segtab is the warp's 32-entry shared-memory table of segment coordinates.
 template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
-                                             int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt) {
+                                             int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt,
+                                             int4* segtab) {
   const unsigned FULL = 0xffffffffu;
   int64_t s = 0, e = 0;
   if (g0 + lane < g1) segs.get(g0 + lane, s, e);
@@ -339,8 +340,14 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   }
   const int total = __shfl_sync(FULL, incl, 31);
   const int excl = incl - nch;
-  probe_group<kKind, kLw, kCap, kW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, incl, edge, c0s - excl,
-                                    total, lane, npos, cnt);
+  const int64_t delta = c0s - excl;
+  __syncwarp();  // the previous group's reads of segtab are done
+  if (lane < nseg)
+    segtab[lane] = make_int4((int)(uint32_t)(uint64_t)delta, (int)(uint32_t)((uint64_t)delta >> 32), excl,
+                             (incl << 5) | edge);
+  __syncwarp();
+  probe_group<kKind, kLw, kCap, kW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab, total, lane, npos,
+                                    cnt);
 }
 
 struct EngineArgs {
@@ -437,8 +444,10 @@ struct Acc {
 template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW>
 __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
+  __shared__ int4 segtabs[kWPB][32];
   const int lane = threadIdx.x & 31;
   WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
+  int4* segtab = segtabs[threadIdx.x >> 5];
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
   for (int i = lane; i < (1 << kLw); i += 32) sl.bm[i] = 0;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         int npos = 0;
         for (int64_t g = ra; g < rb; g += 32)
           stream_group<kExact, kLw, Segs, kTabCap, kW>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                       lane, npos, acc.cnt);
+                                                       lane, npos, acc.cnt, segtab);
         __syncwarp();
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
         __syncwarp();
@@ -501,7 +510,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       int npos = 0;
       for (int64_t g = ra; g < rb; g += 32)
         stream_group<kInline, kLw, Segs, kTabCap, kW>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                      lane, npos, acc.cnt);
+                                                      lane, npos, acc.cnt, segtab);
       __syncwarp();
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
       __syncwarp();
@@ -520,6 +529,9 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
   int4* bkt = reinterpret_cast<int4*>(big_smem + (sizeof(uint32_t) << kLwBig));
   int32_t* pos = reinterpret_cast<int32_t*>(big_smem + (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig)) +
                  (threadIdx.x >> 5) * kPosCap;
+  int4* segtab = reinterpret_cast<int4*>(big_smem + (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
+                                         sizeof(int32_t) * kPosCap * kBigWarps) +
+                 (threadIdx.x >> 5) * 32;
   __shared__ int s_chunk;
   __shared__ int s_next;  // next segment group of the current staged owner (dynamic claiming)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kBigWarps;
@@ -606,10 +618,10 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
           if (g >= rb) break;
           if (staged_exact)
             stream_group<kExact, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
-                                         acc.cnt);
+                                         acc.cnt, segtab);
           else
             stream_group<kBuckets, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
-                                           acc.cnt);
+                                           acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
       } else {
@@ -617,7 +629,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
         int npos = 0;
         for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
           stream_group<kGlobal, 0>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
-                                   acc.cnt);
+                                   acc.cnt, segtab);
       }
     }
     acc.fold();
