@@ -64,8 +64,11 @@ static constexpr int kLwBig = 13;         // block tier filter: 2^13 words = 256
 static constexpr int kLbBig = 11;         // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
 static constexpr int kPosCap = 512;       // block tier: per-warp queue of filter hits
 static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
+static constexpr int kSbWords = 32;  // per-warp bitmap of segment starts: groups of <= 1024 chunks
+static constexpr int kSegTab = 32 + kSbWords / 4;  // int4 per warp: 32 segment entries + the start bitmap
+
 static constexpr size_t kBigSmem = (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
-                                   sizeof(int32_t) * kPosCap * kBigWarps + sizeof(int4) * 32 * kBigWarps;
+                                   sizeof(int32_t) * kPosCap * kBigWarps + sizeof(int4) * kSegTab * kBigWarps;
 static constexpr int kSegCost = 2;        // must match build.cu
 static constexpr int kTabCost = 16;
 static constexpr int32_t kEmpty = -1;
@@ -271,12 +274,14 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 // Segment s covers chunks [excl_s, endx_s) of the flat space; chunk f of it
 // is pool4[delta_s + f]; `edge_s` packs (first-chunk offset | last-chunk
 // count << 2).
-template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin>
+template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
-                                            const int4* __restrict__ segtab, int total, int lane, int& npos,
-                                            uint32_t& cnt) {
+                                            const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
+                                            int total, int lane, int& npos, uint32_t& cnt) {
   const unsigned FULL = 0xffffffffu;
   const bool lane_seg = lane < nseg;
+  const bool fast = kSb && total <= 32 * kSbWords;  // warp-uniform
+  int cbase = 0;                             // fast path: segments starting before the window
   for (int base = 0; base < total; base += 32 * kW) {
     int4 v[kW];
     uint32_t vm[kW];
@@ -286,20 +291,26 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
       vm[k] = 0;
       v[k] = make_int4(0, 0, 0, 0);
       if (b < total) {
-        unsigned cov = __ballot_sync(FULL, lane_seg && excl <= b);
-        int c0 = __popc(cov) - 1;
-        unsigned bit = (lane_seg && excl > b && excl < b + 32) ? (1u << (excl - b)) : 0u;
-        unsigned starts = __reduce_or_sync(FULL, bit);
-        int sj = c0 + __popc(starts & ((2u << lane) - 1u));
-        int f = b + lane;
+        int sj;  // segment of chunk b + lane = (segments starting at or before it) - 1
+        if (fast) {
+          const unsigned starts = sbits[b >> 5];
+          sj = cbase + __popc(starts & ((2u << lane) - 1u)) - 1;
+          cbase += __popc(starts);
+        } else {
+          const unsigned cov = __ballot_sync(FULL, lane_seg && excl <= b);
+          const unsigned bit = (lane_seg && excl > b && excl < b + 32) ? (1u << (excl - b)) : 0u;
+          const unsigned starts = __reduce_or_sync(FULL, bit);
+          sj = __popc(cov) - 1 + __popc(starts & ((2u << lane) - 1u));
+        }
+        const int f = b + lane;
         if (f < total) {
-          const int4 q = segtab[sj];  // (delta lo, delta hi, excl, endx << 5 | edge)
+          const int4 q = segtab[sj];  // (delta lo, delta hi, excl, endx << 8 | last mask << 4 | first mask)
           const int64_t dl = (int64_t)(((uint64_t)(uint32_t)q.y << 32) | (uint32_t)q.x);
-          const int ex = q.z, en = q.w >> 5, eg = q.w & 31;
           v[k] = __ldg(&pool4[dl + f]);
-          uint32_t lo = (f == ex) ? (uint32_t)(eg & 3) : 0u;
-          uint32_t hi = (f == en - 1) ? (uint32_t)(eg >> 2) : 4u;
-          vm[k] = (0xFu >> (4 - hi)) & (0xFu << lo);
+          uint32_t mk = 0xFu;
+          if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
+          if (f == (q.w >> 8) - 1) mk &= ((uint32_t)q.w >> 4) & 0xFu;
+          vm[k] = mk;
         }
       }
     }
@@ -310,8 +321,11 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 }
 
 // One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner;
-// segtab is the warp's 32-entry shared-memory table of segment coordinates.
-template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin>
+// segtab is the warp's shared-memory table (kSegTab int4): 32 segment
+// entries followed by the bitmap of segment starts over the group's chunks.
+// kSb: use the start bitmap (warp tiers; hub groups of the block tier are
+// mostly longer than 1024 chunks and keep the ballot/redux resolution).
+template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt,
                                              int4* segtab) {
@@ -332,7 +346,8 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   // chunk span of each segment: [cs >> 2, (cs + clen + 3) >> 2)
   const int64_t c0s = cs >> 2;
   const int nch = (lane < nseg) ? (int)(((cs + clen + 3) >> 2) - c0s) : 0;
-  const int edge = (int)(cs & 3) | ((int)(((cs + clen - 1) & 3) + 1) << 2);
+  const int fm = (int)((0xFu << (cs & 3)) & 0xFu);            // ids of the first chunk inside the segment
+  const int lm = (int)(0xFu >> (3 - ((cs + clen - 1) & 3)));  // ids of the last chunk inside it
   int incl = nch;
   for (int o = 1; o < 32; o <<= 1) {
     int y = __shfl_up_sync(FULL, incl, o);
@@ -341,13 +356,21 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   const int total = __shfl_sync(FULL, incl, 31);
   const int excl = incl - nch;
   const int64_t delta = c0s - excl;
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(segtab + 32);
+  const bool fast = kSb && total <= 32 * kSbWords;
   __syncwarp();  // the previous group's reads of segtab are done
-  if (lane < nseg)
+  if (lane < nseg) {
     segtab[lane] = make_int4((int)(uint32_t)(uint64_t)delta, (int)(uint32_t)((uint64_t)delta >> 32), excl,
-                             (incl << 5) | edge);
+                             (incl << 8) | (lm << 4) | fm);
+    if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
+  }
   __syncwarp();
-  probe_group<kKind, kLw, kCap, kW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab, total, lane, npos,
-                                    cnt);
+  probe_group<kKind, kLw, kCap, kW, kSb>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab, sbits, total,
+                                         lane, npos, cnt);
+  if (fast) {
+    __syncwarp();
+    if (lane < nseg) sbits[excl >> 5] = 0;
+  }
 }
 
 struct EngineArgs {
@@ -444,10 +467,11 @@ struct Acc {
 template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW>
 __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
-  __shared__ int4 segtabs[kWPB][32];
+  __shared__ int4 segtabs[kWPB][kSegTab];
   const int lane = threadIdx.x & 31;
   WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
   int4* segtab = segtabs[threadIdx.x >> 5];
+  reinterpret_cast<uint32_t*>(segtab + 32)[lane] = 0;  // start bitmap (kSbWords == 32)
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
   for (int i = lane; i < (1 << kLw); i += 32) sl.bm[i] = 0;
@@ -531,12 +555,13 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
                  (threadIdx.x >> 5) * kPosCap;
   int4* segtab = reinterpret_cast<int4*>(big_smem + (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
                                          sizeof(int32_t) * kPosCap * kBigWarps) +
-                 (threadIdx.x >> 5) * 32;
+                 (threadIdx.x >> 5) * kSegTab;
   __shared__ int s_chunk;
   __shared__ int s_next;  // next segment group of the current staged owner (dynamic claiming)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kBigWarps;
   const int nch = *a.nchunks;
   for (int i = threadIdx.x; i < (1 << kLwBig); i += kBigThreads) bm[i] = 0;
+  reinterpret_cast<uint32_t*>(segtab + 32)[lane] = 0;  // start bitmap (kSbWords == 32)
   Acc acc;
   int64_t staged = -1;  // node whose table is staged
   const int32_t* staged_list = nullptr;
@@ -617,10 +642,10 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
           const int64_t g = ra + 32 * (int64_t)gi;
           if (g >= rb) break;
           if (staged_exact)
-            stream_group<kExact, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, false>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
                                          acc.cnt, segtab);
           else
-            stream_group<kBuckets, kLwBig>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, false>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
                                            acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
@@ -628,7 +653,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
         Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1]), 0, 0};
         int npos = 0;
         for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kGlobal, 0>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+          stream_group<kGlobal, 0, Segs, kTabCap, kWin, false>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
                                    acc.cnt, segtab);
       }
     }
