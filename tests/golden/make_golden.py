@@ -219,6 +219,26 @@ def known_answers(tc):
         tc.dedup_send_targets(np.array([3, 4, 9]), np.array([0, 5, 10]), self_rank=0),
     ]
     k["parse"] = parse_cases(tc)
+    # the partitioned schemes on tiny graphs, including more ranks than nodes
+    edge = {}
+    tiny = {"K3": complete(3), "K4": complete(4), "edge": gp([(0, 1)]), "star": gp([(0, 1), (0, 2), (0, 3)]),
+            "empty": gp([])}
+    for name, g in tiny.items():
+        for P in (1, 2, 5):
+            for fn in ("count_space_surrogate", "count_space_direct"):
+                tot, rr = getattr(tc, fn)(g, P, backend="par")
+                edge[f"{name}/{P}/{fn}"] = dict(
+                    total=int(tot), triangles=[int(m.triangles) for m in rr.metrics],
+                    bytes_sent=[int(m.bytes_sent) for m in rr.metrics],
+                    data_msgs_to=[m.data_msgs_to.tolist() for m in rr.metrics],
+                    requests_to=[m.requests_to.tolist() for m in rr.metrics],
+                    partition_bytes=[int(m.partition_bytes) for m in rr.metrics])
+            try:
+                tot, rr = tc.count_dynamic(g, P, backend="par")
+                edge[f"{name}/{P}/count_dynamic"] = dict(total=int(tot), nmetrics=len(rr.metrics))
+            except ValueError as e:
+                edge[f"{name}/{P}/count_dynamic"] = dict(error="ValueError", msg=str(e))
+    k["ranks_edge_cases"] = edge
     k["surrogate_count_k3"] = [
         tc.surrogate_count([], tc.NodeRange(0, 3), k3),
         tc.surrogate_count(k3.succ(0), tc.NodeRange(2, 1), k3),

@@ -531,3 +531,37 @@ def test_direct_cfg1(configs):
             assert [m.triangles for m in mets] == c[f"direct_tri_{P}"]
             assert np.stack([m.requests_to for m in mets]).tolist() == c[f"direct_req_{P}"]
             assert [m.bytes_sent for m in mets] == c[f"direct_bytes_{P}"]
+
+
+_TINY = {"K3": [(a, b) for a in range(3) for b in range(a + 1, 3)],
+         "K4": [(a, b) for a in range(4) for b in range(a + 1, 4)],
+         "edge": [(0, 1)], "star": [(0, 1), (0, 2), (0, 3)], "empty": []}
+
+
+@pytest.mark.parametrize("name", sorted(_TINY))
+def test_partitioned_schemes_tiny_graphs(known, name):
+    """Surrogate / direct / dynamic on tiny graphs, 1, 2 and 5 ranks (more
+    ranks than nodes), single-device and emulated multi-rank, against the
+    reference's outputs (known.json ranks_edge_cases)."""
+    from paper_1406_5687_b200.distributed import emulate_direct_ranks, emulate_ranks
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(_TINY[name])))
+    for P in (1, 2, 5):
+        for fn, emu in (("count_space_surrogate", emulate_ranks), ("count_space_direct", emulate_direct_ranks)):
+            want = known["ranks_edge_cases"][f"{name}/{P}/{fn}"]
+            tot, rr = getattr(tcb, fn)(g, P)
+            tot2, mets = emu(g, P)
+            for t, ms in ((tot, rr.metrics), (tot2, mets)):
+                assert t == want["total"], (fn, P)
+                assert [m.triangles for m in ms] == want["triangles"], (fn, P)
+                assert [m.bytes_sent for m in ms] == want["bytes_sent"], (fn, P)
+                assert [m.data_msgs_to.tolist() for m in ms] == want["data_msgs_to"], (fn, P)
+                assert [m.partition_bytes for m in ms] == want["partition_bytes"], (fn, P)
+                if fn == "count_space_direct":
+                    assert [m.requests_to.tolist() for m in ms] == want["requests_to"], (fn, P)
+        want = known["ranks_edge_cases"][f"{name}/{P}/count_dynamic"]
+        if "error" in want:
+            with pytest.raises(ValueError):
+                tcb.count_dynamic(g, P)
+        else:
+            tot, rr = tcb.count_dynamic(g, P)
+            assert (tot, len(rr.metrics)) == (want["total"], want["nmetrics"])

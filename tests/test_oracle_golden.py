@@ -136,3 +136,23 @@ def test_threaded_tasks_sum_to_total():
     tv = [tv[i] for i in keep]
     tt = [tt[i] for i in keep]
     assert O.count_tasks_threaded(g.eff_indptr, g.eff_indices, tv, tt, 4) == O.count_triangles(g)
+
+
+def test_partitioned_schemes_tiny_graphs_oracle(known):
+    """The oracle's surrogate / direct restatements on tiny graphs with 1, 2
+    and 5 ranks (more ranks than nodes) against the reference's outputs."""
+    tiny = {"K3": [(a, b) for a in range(3) for b in range(a + 1, 3)],
+            "K4": [(a, b) for a in range(4) for b in range(a + 1, 4)],
+            "edge": [(0, 1)], "star": [(0, 1), (0, 2), (0, 3)], "empty": []}
+    for name, pairs in tiny.items():
+        raw = np.asarray(pairs, np.int64).reshape(-1, 2)
+        g = O.build_graph(*O.normalize(raw))
+        for P in (1, 2, 5):
+            b = O.balanced_bounds(O.node_costs(g, "predsum"), 0, g.n, P) if g.n else np.zeros(P + 1, np.int64)
+            sur = known["ranks_edge_cases"][f"{name}/{P}/count_space_surrogate"]
+            partials, census = O.surrogate(g, b)
+            assert partials.tolist() == sur["triangles"] and census.tolist() == sur["data_msgs_to"], (name, P)
+            dire = known["ranks_edge_cases"][f"{name}/{P}/count_space_direct"]
+            dp, dreq, dwords = O.direct(g, b)
+            assert dp.tolist() == dire["triangles"] and dreq.tolist() == dire["requests_to"], (name, P)
+            assert (8 * (2 * dreq.sum(1) + dwords + (P - 1))).tolist() == dire["bytes_sent"], (name, P)
