@@ -84,9 +84,11 @@ struct WarpSliceT {
 
 // --------------------------------------------------------------- segments
 
+// Segment coordinates are int32: pools hold fewer than 2^31 ids (m < 2^31,
+// enforced at build; owner_segments checks its pool).
 struct PullSegs {  // rev_seg int32 pairs (start, end) into the pool
   const int2* seg;
-  __device__ __forceinline__ void get(int64_t r, int64_t& s, int64_t& e) const {
+  __device__ __forceinline__ void get(int64_t r, int& s, int& e) const {
     const int2 x = __ldg(&seg[r]);
     s = x.x;
     e = x.y;
@@ -96,10 +98,10 @@ struct PullSegs {  // rev_seg int32 pairs (start, end) into the pool
 struct PushSegs {  // forward edge e of v -> N^_u, u = indices[e]
   const int64_t* indptr;
   const int32_t* indices;
-  __device__ __forceinline__ void get(int64_t r, int64_t& s, int64_t& e) const {
+  __device__ __forceinline__ void get(int64_t r, int& s, int& e) const {
     int32_t u = __ldg(&indices[r]);
-    s = __ldg(&indptr[u]);
-    e = __ldg(&indptr[u + 1]);
+    s = (int)__ldg(&indptr[u]);
+    e = (int)__ldg(&indptr[u + 1]);
   }
 };
 
@@ -228,8 +230,10 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t off = (uint32_t)(xs[k] - t.tmin);
-      const uint32_t wd = off < t.span ? t.bm[off >> 5] : 0u;
+      // ids outside [tmin, tmin + span) clamp to offset span, whose bit is
+      // never set (span < 32 << lw keeps that word inside the bitmap)
+      const uint32_t off = min((uint32_t)(xs[k] - t.tmin), t.span);
+      const uint32_t wd = t.bm[off >> 5];
       m |= ((wd >> (off & 31)) & 1u) << k;
     }
     cnt += __popc(m & vmask);
@@ -304,9 +308,8 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
         }
         const int f = b + lane;
         if (f < total) {
-          const int4 q = segtab[sj];  // (delta lo, delta hi, excl, endx << 8 | last mask << 4 | first mask)
-          const int64_t dl = (int64_t)(((uint64_t)(uint32_t)q.y << 32) | (uint32_t)q.x);
-          v[k] = __ldg(&pool4[dl + f]);
+          const int4 q = segtab[sj];  // (delta, -, excl, endx << 8 | last mask << 4 | first mask)
+          v[k] = __ldg(&pool4[q.x + f]);
           uint32_t mk = 0xFu;
           if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
           if (f == (q.w >> 8) - 1) mk &= ((uint32_t)q.w >> 4) & 0xFu;
@@ -330,9 +333,9 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
                                              int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt,
                                              int4* segtab) {
   const unsigned FULL = 0xffffffffu;
-  int64_t s = 0, e = 0;
+  int s = 0, e = 0;
   if (g0 + lane < g1) segs.get(g0 + lane, s, e);
-  int len = (int)(e - s);
+  int len = e - s;
   unsigned nz = __ballot_sync(FULL, len > 0);  // compact non-empty segments to the low lanes
   int nseg = __popc(nz);
   // rows keep non-empty segments first (build.cu k_rev_scatter; owner
@@ -340,12 +343,12 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   // prefix and the compaction is the identity
   int src = lane;
   if (nz & (nz + 1u)) src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
-  int64_t cs = __shfl_sync(FULL, s, src);
+  int cs = __shfl_sync(FULL, s, src);
   int clen = __shfl_sync(FULL, len, src);
   if (lane >= nseg) clen = 0;
   // chunk span of each segment: [cs >> 2, (cs + clen + 3) >> 2)
-  const int64_t c0s = cs >> 2;
-  const int nch = (lane < nseg) ? (int)(((cs + clen + 3) >> 2) - c0s) : 0;
+  const int c0s = cs >> 2;
+  const int nch = (lane < nseg) ? ((cs + clen + 3) >> 2) - c0s : 0;
   const int fm = (int)((0xFu << (cs & 3)) & 0xFu);            // ids of the first chunk inside the segment
   const int lm = (int)(0xFu >> (3 - ((cs + clen - 1) & 3)));  // ids of the last chunk inside it
   int incl = nch;
@@ -355,13 +358,12 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   }
   const int total = __shfl_sync(FULL, incl, 31);
   const int excl = incl - nch;
-  const int64_t delta = c0s - excl;
+  const int delta = c0s - excl;  // chunk f of the segment is pool4[delta + f]
   uint32_t* sbits = reinterpret_cast<uint32_t*>(segtab + 32);
   const bool fast = kSb && total <= 32 * kSbWords;
   __syncwarp();  // the previous group's reads of segtab are done
   if (lane < nseg) {
-    segtab[lane] = make_int4((int)(uint32_t)(uint64_t)delta, (int)(uint32_t)((uint64_t)delta >> 32), excl,
-                             (incl << 8) | (lm << 4) | fm);
+    segtab[lane] = make_int4(delta, 0, excl, (incl << 8) | (lm << 4) | fm);
     if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
   }
   __syncwarp();
@@ -495,13 +497,14 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       const OwnerRef ow = resolve_owner(a, x);
       const int64_t u = ow.u;
       const int64_t t0 = __ldg(&a.tab_indptr[u]);
-      const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d <= a.d_lo || d > a.d_hi) continue;
+      const int64_t d64 = __ldg(&a.tab_indptr[u + 1]) - t0;
+      if (d64 <= a.d_lo || d64 > a.d_hi) continue;
+      const int d = (int)d64;  // <= the tier cap
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + t0;
       const int32_t tlo = __ldg(&gtab[0]);
       const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
-      if (span <= (32u << kLw)) {
+      if (span < (32u << kLw)) {
         // Narrow id span (hub owners at the top of the degree order): the
         // filter words become an exact direct-mapped bitmap over [tlo, tlo+span).
         for (int i = lane; i < d; i += 32) {
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
           }
           const int32_t tlo = __ldg(&gtab[0]);
           const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
-          const bool exact = span <= (32u << kLwBig);
+          const bool exact = span < (32u << kLwBig);
           if (!exact)
             for (int i = threadIdx.x; i < (1 << lb); i += kBigThreads) bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncthreads();
@@ -810,7 +813,7 @@ __global__ void k_seg_cost(const int32_t* __restrict__ own, const int64_t* __res
     const int64_t d = tab_indptr[u + 1] - tab_indptr[u];
     const int64_t r0 = vrow[x], r1 = vrow[x + 1], p0 = phys_row[o];
     for (int64_t r = r0 + lane; r < r1; r += 32) {
-      int64_t s = 0, e = 0;
+      int s = 0, e = 0;
       segs.get(p0 + (r - r0), s, e);
       cost[r] = (e - s) + kSegCost + (r == r0 ? d + kTabCost : 0);
     }
