@@ -243,8 +243,10 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t h = tab_hash((uint32_t)xs[k]);
-    const uint32_t mk = filt_mask<kLw>(h);
-    m |= ((t.bm[h >> (32 - kLw)] & mk) == mk ? 1u : 0u) << k;
+    // bit (h >> (27 - lw)) & 31 of word h >> (32 - lw): the funnel shift
+    // takes its amount mod 32, so no mask is needed
+    const uint32_t wd = t.bm[h >> (32 - kLw)];
+    m |= (__funnelshift_r(wd, wd, h >> (27 - kLw)) & 1u) << k;
   }
   m &= vmask;
   if (kKind == kInline) {
