@@ -104,7 +104,7 @@ int or_normalize(const int64_t *edges, int64_t m_raw, int64_t *out_edges,
     }
     free(key);
     free(pos);
-    if (K != uniq[K - 1] + 1) {
+    if (K > 0 && K != uniq[K - 1] + 1) {
         /* new_id[argsort(first_pos, stable)] = arange(K)   (graph.py:96-97) */
         uint64_t *fk = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)K);
         int64_t *fi = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
