@@ -163,18 +163,25 @@ __global__ void k_unpack_pairs(const unsigned long long* __restrict__ keys, int6
   }
 }
 
-// Degree histogram over the pair list (thread per pair, run-aggregated).
-__global__ void k_histogram(const int32_t* __restrict__ ids, int64_t npairs, int32_t* h) {
+// Degree histogram over the pair list (thread per pair, run-aggregated),
+// fused with the endpoint range check: out-of-range ids set `bad` (bit 0
+// negative, bit 1 >= n) and are not counted.
+__global__ void k_histogram(const int32_t* __restrict__ ids, int64_t npairs, int64_t n, int32_t* h, int* bad) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int flags = 0;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < npairs;
-    const int2 p = valid ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
+    int2 p = valid ? reinterpret_cast<const int2*>(ids)[i] : make_int2(0, 0);
+    const bool okx = p.x >= 0 && (int64_t)p.x < n, oky = p.y >= 0 && (int64_t)p.y < n;
+    flags |= (p.x < 0 || p.y < 0 ? 1 : 0) | ((int64_t)p.x >= n || (int64_t)p.y >= n ? 2 : 0);
     int st = 0, c;
-    if ((c = warp_run_end(p.x, valid, lane, &st))) atomicAdd(&h[p.x], c);
-    if ((c = warp_run_end(p.y, valid, lane, &st))) atomicAdd(&h[p.y], c);
+    if ((c = warp_run_end(p.x, valid && okx, lane, &st))) atomicAdd(&h[p.x], c);
+    if ((c = warp_run_end(p.y, valid && oky, lane, &st))) atomicAdd(&h[p.y], c);
   }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lane == 0 && flags) atomicOr(bad, flags);
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -185,36 +192,51 @@ __global__ void k_copy_i32(const int32_t* __restrict__ a, int32_t* b, int64_t n)
   GRID_STRIDE(i, n) b[i] = a[i];
 }
 
-__global__ void k_range_check(const int32_t* __restrict__ ids, int64_t cnt, int64_t n, int* bad) {
-  GRID_STRIDE(i, cnt) {
-    int x = ids[i];
-    if (x < 0) atomicOr(bad, 1);
-    else if ((int64_t)x >= n) atomicOr(bad, 2);
-  }
-}
 
-// Per-row entry counts from row keys sorted ascending: the first entry of a
-// row subtracts its index, the last adds index+1 (two uncontended atomics
-// per non-empty row); an exclusive scan then gives the CSR offsets.
-template <class RowOf>
-__global__ void k_row_counts(RowOf row_of, int64_t m, long long* cnt) {
+// Orientation (graph.py:113-125), counting-sort form.  Pass 1: every pair
+// becomes (lo, hi) in canonical labels (kept for pass 2) and adds 1 to row
+// lo's size (fire-and-forget atomics).
+__global__ void k_orient_count(const int32_t* __restrict__ e, int64_t m, const int32_t* __restrict__ relabel,
+                               int2* __restrict__ lohi, unsigned long long* cnt) {
   GRID_STRIDE(i, m) {
-    int64_t r = row_of(i);
-    if (i == 0 || row_of(i - 1) != r) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[r]), (unsigned long long)(-(long long)i));
-    if (i == m - 1 || row_of(i + 1) != r) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[r]), (unsigned long long)(i + 1));
+    const int2 p = reinterpret_cast<const int2*>(e)[i];
+    const int32_t x = relabel[p.x], y = relabel[p.y];
+    const int2 k = make_int2(min(x, y), max(x, y));
+    lohi[i] = k;
+    atomicAdd(&cnt[k.x], 1ull);
   }
 }
 
-struct RowHi {  // row of a packed (lo << b | hi) key = lo
-  const unsigned long long* k;
-  int b;
-  __device__ int64_t operator()(int64_t i) const { return (int64_t)(k[i] >> b); }
-};
+// Pass 2: hi goes to a slot of row lo claimed with an atomic cursor.  The
+// scatter runs in phases over row ranges [bounds[ph], bounds[ph+1]) whose
+// slots span about the same number of entries, so each phase's writes land
+// in an L2-resident window of the output instead of random DRAM sectors.
+__global__ void k_orient_scatter(const int2* __restrict__ lohi, int64_t m, const int64_t* __restrict__ indptr,
+                                 const int64_t* __restrict__ bounds, int ph, int32_t* cursor, int32_t* out) {
+  const int64_t r0 = bounds[ph], r1 = bounds[ph + 1];
+  GRID_STRIDE(i, m) {
+    const int2 k = lohi[i];
+    if (k.x >= r0 && k.x < r1) out[indptr[k.x] + atomicAdd(&cursor[k.x], 1)] = k.y;
+  }
+}
 
-__global__ void k_eff_indices(const unsigned long long* __restrict__ keys, int64_t m, int b,
-                              int32_t* eff_indices) {
-  unsigned long long mask = (1ull << b) - 1;
-  GRID_STRIDE(i, m) eff_indices[i] = (int32_t)(keys[i] & mask);
+// Row boundaries of `nph` phases holding about equal shares of the
+// indptr[n] entries (thread per boundary, binary search).
+__global__ void k_phase_bounds(const int64_t* __restrict__ indptr, int64_t n, int nph, int64_t* bounds) {
+  const int p = threadIdx.x;
+  if (p > nph) return;
+  if (p == 0 || p == nph) {
+    bounds[p] = p == 0 ? 0 : n;
+    return;
+  }
+  const int64_t target = (int64_t)((__int128)indptr[n] * p / nph);
+  int64_t lo = 0, hi = n;  // first row whose start is >= target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (indptr[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[p] = lo;
 }
 
 // deg / eff_deg of the canonical nodes, and the in-degree (number of
@@ -231,25 +253,133 @@ __global__ void k_degrees(const int64_t* __restrict__ indptr, const int32_t* __r
   }
 }
 
-// Reverse CSR by counting scatter: edge i = (v, u) of the forward list
-// (keys sorted by (v, u)) goes to a slot of row u claimed with an atomic
-// cursor -- non-empty suffixes from the front of the row, empty ones (u is
-// the last id of N^_v) from the back, so the engine's segment groups are
-// prefix-dense and need no compaction.  Order within those two parts is
-// unspecified (the pull engine only sums over a row); the full CSR sorts
-// its rows when it is assembled.
-__global__ void k_rev_scatter(const unsigned long long* __restrict__ keys, int64_t m, int b,
-                              const int64_t* __restrict__ eff_indptr, const int64_t* __restrict__ rev_indptr,
-                              int32_t* cursor, int32_t* back, int2* rev_seg) {
-  const unsigned long long mask = (1ull << b) - 1;
-  GRID_STRIDE(i, m) {
-    const unsigned long long k = keys[i];
-    const int64_t v = (int64_t)(k >> b), u = (int64_t)(k & mask);
-    const int64_t end = eff_indptr[v + 1];
-    const int64_t slot = (i + 1 < end) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
-                                       : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
-    rev_seg[slot] = make_int2((int)(i + 1), (int)end);
+// Reverse CSR by counting scatter: forward edge e = (v, u) goes to a slot
+// of row u claimed with an atomic cursor -- non-empty suffixes from the
+// front of the row, empty ones (u is the last id of N^_v) from the back, so
+// the engine's segment groups are prefix-dense and need no compaction.
+// Order within those two parts is unspecified (the pull engine only sums
+// over a row); the full CSR sorts its rows when it is assembled.  A warp
+// takes kRevSpan consecutive forward edges (coalesced reads whatever the
+// row lengths); each lane walks from the chunk's first row to its own.
+// Phased over destination rows like k_orient_scatter.
+static constexpr int kRevSpan = 1024;
+__global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
+                              int64_t n, int64_t m, const int64_t* __restrict__ rev_indptr,
+                              const int64_t* __restrict__ bounds, int ph, int32_t* cursor, int32_t* back,
+                              int2* rev_seg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t u0 = bounds[ph], u1 = bounds[ph + 1];
+  for (int64_t e0 = warp * kRevSpan; e0 < m; e0 += nwarps * kRevSpan) {
+    const int64_t e1 = min(m, e0 + kRevSpan);
+    int64_t v = row_of_edge(eff_indptr, n, e0);
+    int64_t vend = eff_indptr[v + 1];
+    for (int64_t c = e0; c < e1; c += 32) {
+      const int64_t e = min(c + lane, e1 - 1);
+      int64_t w = v, wend = vend;
+      while (wend <= e) wend = eff_indptr[++w + 1];
+      v = __shfl_sync(0xffffffffu, w, 31);
+      vend = __shfl_sync(0xffffffffu, wend, 31);
+      if (c + lane >= e1) continue;
+      const int64_t u = eff_indices[e];
+      if (u < u0 || u >= u1) continue;
+      const int64_t slot = (e + 1 < wend) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
+                                          : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
+      rev_seg[slot] = make_int2((int)(e + 1), (int)wend);
+    }
   }
+}
+
+// Row sorts after the counting scatter.  CUB's segmented sort handles rows
+// of at most kCubRowMax ids with sub-warp merge sorts (fast) and larger
+// ones with one block-wide radix sort per row (slow when there are many,
+// e.g. dense ER rows of 100-400: 68 ms at cfg 5).  Rows in (kCubRowMax,
+// kBlockRowMax] are sorted here instead -- a warp per row up to 1 024 ids
+// (merge sorts of 8 / 16 / 32 keys per lane), a block per row above (256 x 8
+// or 512 x 16 keys) -- and
+// are handed to CUB as empty segments.
+static constexpr int kCubRowMax = 112;  // CUB's sm_100 (Policy860) medium tile: 16 threads x 7 keys
+static constexpr int kBlockRowMax = 8192;
+
+__global__ void k_row_classes(const int64_t* __restrict__ indptr, int64_t n, int64_t* seg_end, int32_t* rows,
+                              int64_t cap, int* counts) {
+  GRID_STRIDE(v, n) {
+    const int64_t b = indptr[v], e = indptr[v + 1], L = e - b;
+    const int cls = L <= kCubRowMax ? -1
+                    : L <= 256 ? 0 : L <= 512 ? 1 : L <= 1024 ? 2 : L <= 2048 ? 3 : L <= kBlockRowMax ? 4 : -1;
+    seg_end[v] = cls < 0 ? e : b;
+    if (cls >= 0) rows[cls * cap + atomicAdd(&counts[cls], 1)] = (int32_t)v;
+  }
+}
+
+struct LessI32 {
+  __device__ bool operator()(const int32_t& a, const int32_t& b) const { return a < b; }
+};
+
+template <int kIpt>
+__global__ void __launch_bounds__(256) k_sort_rows_warp(const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ in, int32_t* out,
+                                                        const int32_t* __restrict__ rows, const int* count) {
+  using WS = cub::WarpMergeSort<int32_t, kIpt, 32>;
+  __shared__ typename WS::TempStorage tmp[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int cnt = *count;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < cnt; r += nwarps) {
+    const int32_t v = rows[r];
+    const int64_t b = indptr[v];
+    const int L = (int)(indptr[v + 1] - b);
+    int32_t k[kIpt];
+#pragma unroll
+    for (int i = 0; i < kIpt; ++i) {
+      const int idx = i * 32 + lane;  // striped load (coalesced) ...
+      k[i] = idx < L ? in[b + idx] : INT_MAX;
+    }
+    WS(tmp[wid]).Sort(k, LessI32());  // ... blocked result: lane holds ranks lane*kIpt + i
+#pragma unroll
+    for (int i = 0; i < kIpt; ++i) {
+      const int idx = lane * kIpt + i;
+      if (idx < L) out[b + idx] = k[i];
+    }
+    __syncwarp();
+  }
+}
+
+template <int kThreads, int kIpt>
+__global__ void __launch_bounds__(kThreads) k_sort_rows_block(const int64_t* __restrict__ indptr,
+                                                              const int32_t* __restrict__ in, int32_t* out,
+                                                              const int32_t* __restrict__ rows, const int* count) {
+  using BS = cub::BlockMergeSort<int32_t, kThreads, kIpt>;
+  __shared__ typename BS::TempStorage tmp;
+  const int cnt = *count;
+  for (int r = blockIdx.x; r < cnt; r += gridDim.x) {
+    const int32_t v = rows[r];
+    const int64_t b = indptr[v];
+    const int L = (int)(indptr[v + 1] - b);
+    int32_t k[kIpt];
+#pragma unroll
+    for (int i = 0; i < kIpt; ++i) {
+      const int idx = i * kThreads + threadIdx.x;
+      k[i] = idx < L ? in[b + idx] : INT_MAX;
+    }
+    BS(tmp).Sort(k, LessI32());
+#pragma unroll
+    for (int i = 0; i < kIpt; ++i) {
+      const int idx = threadIdx.x * kIpt + i;
+      if (idx < L) out[b + idx] = k[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Phase count for a scatter of `bytes` of output: enough phases that each
+// window fits comfortably in L2 (64 MB), when at most 4 do (every phase
+// re-reads the source); otherwise one.
+inline int scatter_phases(int64_t bytes) {
+  const int64_t window = 64ll << 20;
+  const int64_t p = (bytes + window - 1) / window;
+  return p <= 4 ? (int)std::max<int64_t>(1, p) : 1;
 }
 
 // Warp per u: pull-engine cost of u (see kSegCost / kTabCost).
@@ -332,22 +462,6 @@ void sort_pairs(Scratch& sc, K*& ka, K* kb, V*& va, V* vb, int64_t n, int end_bi
   va = dv.Current();
 }
 
-
-template <class RowOf>
-void indptr_from_sorted(Scratch& sc, RowOf row_of, int64_t m, int64_t n, int64_t* indptr,
-                        cudaStream_t s) {
-  long long* cnt = sc.alloc<long long>(n + 1);
-  TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(long long), s));
-  if (m) {
-    k_row_counts<<<grid_for(m, kBlock, sm_count() * 16), kBlock, 0, s>>>(row_of, m, cnt);
-    check_launch();
-  }
-  size_t tmp = 0;
-  long long* out = reinterpret_cast<long long*>(indptr);
-  TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, out, n + 1, s));
-  void* t = sc.bytes(tmp);
-  TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cnt, out, n + 1, s));
-}
 
 template <class T>
 T read_scalar(const T* d, cudaStream_t s) {
@@ -469,11 +583,14 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   TC_REQUIRE(m < (1ll << 31) - 1, TC_EINVAL, "m must be < 2^31");
   Scratch sc(s);
   int sms = sm_count();
+  // degrees (graph.py:149-151), with the endpoint range check
+  int32_t* deg_orig = sc.alloc<int32_t>(n);
+  if (n) TC_CUDA(cudaMemsetAsync(deg_orig, 0, n * sizeof(int32_t), s));
   if (m > 0) {
     TC_REQUIRE(((uintptr_t)edges & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
     int* bad = sc.alloc<int>(1);
     TC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-    k_range_check<<<grid_for(2 * m, kBlock, sms * 8), kBlock, 0, s>>>(edges, 2 * m, n, bad);
+    k_histogram<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, n, deg_orig, bad);
     check_launch();
     int hb = read_scalar(bad, s);
     TC_REQUIRE(!(hb & 1), TC_EINVAL, "negative node id in edge list");
@@ -484,13 +601,6 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     TC_CUDA(cudaMemsetAsync(rev_indptr, 0, sizeof(int64_t), s));
     TC_CUDA(cudaMemsetAsync(rev_cost, 0, sizeof(int64_t), s));
     return;
-  }
-  // degrees (graph.py:149-151)
-  int32_t* deg_orig = sc.alloc<int32_t>(n);
-  TC_CUDA(cudaMemsetAsync(deg_orig, 0, n * sizeof(int32_t), s));
-  if (m) {
-    k_histogram<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, deg_orig);
-    check_launch();
   }
   // canonical order: ascending (degree, id) via a stable radix sort (graph.py:152)
   if (order) {
@@ -510,19 +620,60 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   k_rank_scatter<<<grid_for(n, kBlock), kBlock, 0, s>>>(orig_ids, n, relabel);  // graph.py:111-112
   check_launch();
 
-  // orientation + forward CSR (graph.py:113-124)
-  int b = std::max(1, bits_for((uint64_t)(n - 1)));
-  auto* ka = sc.alloc<unsigned long long>(m);
-  auto* kb = sc.alloc<unsigned long long>(m);
-  if (m) {
-    k_pack_pairs<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, b, ka, nullptr);
-    check_launch();
-  }
-  unsigned long long* keys = sort_keys(sc, ka, kb, m, 2 * b, s);
-  indptr_from_sorted(sc, RowHi{keys, b}, m, n, eff_indptr, s);
-  if (m) {
-    k_eff_indices<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indices);
-    check_launch();
+  // orientation + forward CSR (graph.py:113-124): row sizes, offsets,
+  // phased counting scatter, then every row sorted (segmented sort)
+  int64_t* bounds = sc.alloc<int64_t>(8);
+  {
+    unsigned long long* cnt = sc.alloc<unsigned long long>(n + 1);
+    TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(unsigned long long), s));
+    int2* lohi = sc.alloc<int2>(m);
+    if (m) {
+      k_orient_count<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, lohi, cnt);
+      check_launch();
+    }
+    size_t tmp = 0;
+    auto* cin = reinterpret_cast<long long*>(cnt);
+    auto* cout = reinterpret_cast<long long*>(eff_indptr);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cin, cout, n + 1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cin, cout, n + 1, s));
+    if (m) {
+      int32_t* unsorted = sc.alloc<int32_t>(m);
+      int32_t* cursor = sc.alloc<int32_t>(n);
+      TC_CUDA(cudaMemsetAsync(cursor, 0, n * sizeof(int32_t), s));
+      const int nph = scatter_phases(m * 4);
+      k_phase_bounds<<<1, 32, 0, s>>>(eff_indptr, n, nph, bounds);
+      check_launch();
+      for (int ph = 0; ph < nph; ++ph) {
+        k_orient_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(lohi, m, eff_indptr, bounds, ph, cursor,
+                                                                          unsorted);
+        check_launch();
+      }
+      TC_REQUIRE(m < (1ll << 31), TC_EINVAL, "m must be < 2^31");
+      int64_t* seg_end = sc.alloc<int64_t>(n);
+      int32_t* rows = sc.alloc<int32_t>(5 * n);
+      int* counts = sc.alloc<int>(5);
+      TC_CUDA(cudaMemsetAsync(counts, 0, 5 * sizeof(int), s));
+      k_row_classes<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, n, seg_end, rows, n, counts);
+      check_launch();
+      size_t tmp2 = 0;
+      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp2, unsorted, eff_indices, (int)m, (int)n, eff_indptr,
+                                                 seg_end, s));
+      void* t2 = sc.bytes(tmp2);
+      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(t2, tmp2, unsorted, eff_indices, (int)m, (int)n, eff_indptr,
+                                                 seg_end, s));
+      k_sort_rows_warp<8><<<sms * 8, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows, counts);
+      check_launch();
+      k_sort_rows_warp<16><<<sms * 8, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + n, counts + 1);
+      check_launch();
+      k_sort_rows_warp<32><<<sms * 4, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + 2 * n, counts + 2);
+      check_launch();
+      k_sort_rows_block<256, 8><<<sms * 4, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + 3 * n, counts + 3);
+      check_launch();
+      k_sort_rows_block<512, kBlockRowMax / 512><<<sms * 2, 512, 0, s>>>(eff_indptr, unsorted, eff_indices,
+                                                                         rows + 4 * n, counts + 4);
+      check_launch();
+    }
   }
   int64_t* in_deg = sc.alloc<int64_t>(n + 1);
   TC_CUDA(cudaMemsetAsync(in_deg + n, 0, sizeof(int64_t), s));
@@ -539,9 +690,14 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   if (m) {
     int32_t* cursor = sc.alloc<int32_t>(2 * n);
     TC_CUDA(cudaMemsetAsync(cursor, 0, 2 * n * sizeof(int32_t), s));
-    k_rev_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(keys, m, b, eff_indptr, rev_indptr, cursor,
-                                                                   cursor + n, reinterpret_cast<int2*>(rev_seg));
+    const int nph = scatter_phases(m * 8);
+    k_phase_bounds<<<1, 32, 0, s>>>(rev_indptr, n, nph, bounds);
     check_launch();
+    for (int ph = 0; ph < nph; ++ph) {
+      k_rev_scatter<<<grid_for((m + kRevSpan - 1) / kRevSpan * 32, kBlock, sms * 16), kBlock, 0, s>>>(
+          eff_indptr, eff_indices, n, m, rev_indptr, bounds, ph, cursor, cursor + n, reinterpret_cast<int2*>(rev_seg));
+      check_launch();
+    }
   }
   // pull-engine cost prefix over u
   int64_t* cu = sc.alloc<int64_t>(n + 1);

@@ -360,6 +360,34 @@ def test_dense_core_block_tier():
     assert [m.triangles for m in rr.metrics] == partials.tolist()
 
 
+def test_build_row_sort_classes():
+    """Forward rows of every length class the build sorts differently (CUB
+    sub-warp sorts <= 112, warp merge sorts <= 256 / 512 / 1024, block merge
+    sorts <= 2048 / 8192, CUB block radix sort above), in the degree order (dense
+    cores) and in the identity order (hubs with low ids); every field
+    against the oracle."""
+    rng = np.random.default_rng(11)
+    chain = np.arange(20000)
+    parts = [np.stack([chain[:-1], chain[1:]], 1), rng.integers(0, 20000, size=(60000, 2))]  # dense labels
+    for hub, size in ((0, 9000), (1, 5000), (2, 900), (3, 450), (4, 300), (5, 200), (6, 120), (7, 1500)):
+        parts.append(np.stack([np.full(size, hub), rng.choice(np.arange(8, 20000), size, replace=False)], 1))
+    core = rng.choice(np.arange(20000), 700, replace=False)  # K_700: degree-order rows up to 699
+    a, b = np.triu_indices(700, 1)
+    parts.append(np.stack([core[a], core[b]], 1))
+    raw = np.concatenate(parts).astype(np.int64)
+    on, oe = O.normalize(raw)
+    norm = tcb.normalize(tcb.RawGraph.from_pairs(raw))
+    for order in (None, np.arange(on, dtype=np.int64)):
+        og = O.build_graph(on, oe, order=order)
+        g = tcb.build_graph(norm) if order is None else G._build_graph_input_order(norm)
+        lens = np.diff(og.eff_indptr)
+        assert lens.max() > 1024 if order is not None else lens.max() > 512
+        for f in ("eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg",
+                  "full_indptr", "full_indices"):
+            assert np.array_equal(host(getattr(g, f)), getattr(og, f)), f
+        assert tcb.count_triangles_seq(g) == O.count_triangles(og)
+
+
 @pytest.mark.parametrize("name", ["er_60_0.2_21", "pa_1500_12_3", "sparse_labels", "rmat_s10", "gnm_2000_16000", "k9"])
 def test_multi_rank_path_emulated(name):
     """The per-rank device kernels of the multi-GPU surrogate protocol
