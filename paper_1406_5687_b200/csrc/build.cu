@@ -39,11 +39,6 @@ __global__ void k_minmax(const int32_t* __restrict__ a, int64_t cnt, int* mn, in
   }
 }
 
-struct NotSelfLoop {
-  __host__ __device__ bool operator()(const unsigned long long& x) const {
-    return (uint32_t)(x & 0xFFFFFFFFull) != (uint32_t)(x >> 32);
-  }
-};
 
 // Run aggregation for scattered atomics: lanes of a warp that hold equal
 // keys in consecutive lanes form a run; the run's last lane gets its length
@@ -63,15 +58,18 @@ __device__ __forceinline__ int warp_run_end(int32_t key, bool valid, int lane, i
   return lane - *start + 1;
 }
 
-// First position of every label in the raveled pair list (thread per pair;
-// the two endpoint columns are aggregated separately).
+// First position of every label in the raveled pair list, self-loops
+// excluded (thread per pair; the two endpoint columns are aggregated
+// separately).  Positions count the raw list, self-loops included: the
+// relative order of the remaining pairs -- all the first-seen ranks depend
+// on -- is the same as after graph.py:89 drops them.
 __global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t npairs, uint32_t* fp) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
-    const bool valid = i < npairs;
-    const int2 p = valid ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
+    const int2 p = i < npairs ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
+    const bool valid = i < npairs && p.x != p.y;
     int st = 0;
     if (warp_run_end(p.x, valid, lane, &st)) atomicMin(&fp[p.x], (uint32_t)(2 * (i - lane + st)));
     if (warp_run_end(p.y, valid, lane, &st)) atomicMin(&fp[p.y], (uint32_t)(2 * (i - lane + st) + 1));
@@ -115,14 +113,13 @@ __global__ void k_rank_scatter(const int32_t* __restrict__ ids, int64_t cnt, int
   GRID_STRIDE(i, cnt) new_id[ids[i]] = (int32_t)i;
 }
 
-__global__ void k_remap(int32_t* ids, int64_t cnt, const int32_t* __restrict__ new_id) {
-  GRID_STRIDE(i, cnt) ids[i] = new_id[ids[i]];
-}
-
-// (min, max) of each pair packed as lo << b | hi; optional relabel map.
+// (min, max) of each pair packed as lo << b | hi; optional relabel map.  A
+// self-loop packs as the sentinel (mask, mask), above every real pair
+// (min < max), so it sorts last and is dropped after the unique pass.
 __device__ __forceinline__ unsigned long long pair_key(const int32_t* __restrict__ e, int64_t i,
                                                      const int32_t* __restrict__ relabel, int b) {
   int32_t x = e[2 * i], y = e[2 * i + 1];
+  if (x == y) return (2ull << (2 * b - 1)) - 1;
   if (relabel) {
     x = relabel[x];
     y = relabel[y];
@@ -493,26 +490,12 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   sync_stream(s);
   TC_REQUIRE(hmm[0] >= 0, TC_EINVAL, "negative node id in edge list");  // graph.py:87-88
 
-  // drop self-loops (graph.py:89)
-  auto* e1 = sc.alloc<unsigned long long>(m_raw);
-  auto* nsel = sc.alloc<long long>(1);
-  {
-    size_t tmp = 0;
-    auto in = reinterpret_cast<const unsigned long long*>(edges);
-    TC_CUDA(cub::DeviceSelect::If(nullptr, tmp, in, e1, nsel, m_raw, NotSelfLoop(), s));
-    void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceSelect::If(t, tmp, in, e1, nsel, m_raw, NotSelfLoop(), s));
-  }
-  int64_t m1 = read_scalar(nsel, s);
-  if (m1 == 0) return;  // graph.py:90-91
-  int32_t* ids = reinterpret_cast<int32_t*>(e1);
-  int64_t nid = 2 * m1;
-  int64_t L1 = (int64_t)hmm[1] + 1;
-
-  // first occurrence of each label in the raveled order (graph.py:92-93)
+  // first occurrence of each label in the raveled order, self-loops
+  // excluded (graph.py:89-93)
+  const int64_t L1 = (int64_t)hmm[1] + 1;
   uint32_t* fp = sc.alloc<uint32_t>(L1);
   TC_CUDA(cudaMemsetAsync(fp, 0xFF, L1 * sizeof(uint32_t), s));
-  k_first_pos<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, fp);
+  k_first_pos<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(edges, m_raw, fp);
   check_launch();
   auto* cnt = sc.alloc<unsigned long long>(1);
   int* lf = sc.alloc<int>(1);
@@ -523,6 +506,9 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   check_launch();
   int64_t K = (int64_t)read_scalar(cnt, s);
   int64_t Lf = read_scalar(lf, s);
+  if (K == 0) return;  // only self-loops (graph.py:90-91)
+  auto* nsel = sc.alloc<long long>(1);
+  const int32_t* relabel = nullptr;
 
   if (K != Lf + 1) {
     // first-seen compaction (graph.py:96-98): new id = rank of first position
@@ -540,31 +526,36 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
     uint32_t* fk2 = sc.alloc<uint32_t>(K);
     k_gather_u32<<<grid_for(K, kBlock), kBlock, 0, s>>>(pid, fp, K, fk);
     check_launch();
-    sort_pairs(sc, fk, fk2, pid, pid2, K, bits_for((uint64_t)nid), s);
+    sort_pairs(sc, fk, fk2, pid, pid2, K, bits_for((uint64_t)(2 * m_raw)), s);
     int32_t* new_id = reinterpret_cast<int32_t*>(fp);  // fp no longer needed
     k_rank_scatter<<<grid_for(K, kBlock), kBlock, 0, s>>>(pid, K, new_id);
     check_launch();
-    k_remap<<<grid_for(nid, kBlock, sms * 16), kBlock, 0, s>>>(ids, nid, new_id);
-    check_launch();
+    relabel = new_id;
   }
 
   // (lo, hi) + unique rows (graph.py:99-102)
   int b = std::max(1, bits_for((uint64_t)(K - 1)));
-  auto* ka = sc.alloc<unsigned long long>(m1);
-  auto* kb = sc.alloc<unsigned long long>(m1);
+  auto* ka = sc.alloc<unsigned long long>(m_raw);
+  auto* kb = sc.alloc<unsigned long long>(m_raw);
   unsigned* oflags = sc.alloc<unsigned>(1);
   TC_CUDA(cudaMemsetAsync(oflags, 0, sizeof(unsigned), s));
-  k_pack_pairs<<<grid_for(m1, kBlock, sms * 16), kBlock, 0, s>>>(ids, m1, nullptr, b, ka, oflags);
+  k_pack_pairs<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(edges, m_raw, relabel, b, ka, oflags);
   check_launch();
-  unsigned long long* sorted = sort_packed(sc, ka, kb, m1, b, oflags, s);
+  unsigned long long* sorted = sort_packed(sc, ka, kb, m_raw, b, oflags, s);
   unsigned long long* uniq = (sorted == ka) ? kb : ka;
   {
     size_t tmp = 0;
-    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel, m1, s));
+    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel, m_raw, s));
     void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, uniq, nsel, m1, s));
+    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, uniq, nsel, m_raw, s));
   }
   int64_t m2 = read_scalar(nsel, s);
+  {  // drop the self-loop sentinel (sorted last) if there was one
+    unsigned long long last = 0;
+    TC_CUDA(cudaMemcpyAsync(&last, uniq + m2 - 1, sizeof(last), cudaMemcpyDeviceToHost, s));
+    sync_stream(s);
+    if (last == (2ull << (2 * b - 1)) - 1) --m2;
+  }
   k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, b, out_edges);
   check_launch();
   sync_stream(s);
