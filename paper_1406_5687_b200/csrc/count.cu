@@ -449,20 +449,43 @@ struct EngineArgs {
   // [row_indptr[x], row_indptr[x+1]) are physical [phys_row[o], ...).
   const int32_t* tier_owner;
   const int64_t* phys_row;
+  // Owner descriptors, built with the plan: everything the engine needs to
+  // stage an owner's table in two independent 16-byte loads instead of a
+  // chain of dependent ones (tier_owner -> phys_row / owner_map ->
+  // tab_indptr -> first / last table id).
+  const int4* desc_a;       // (u, d, first id, id span)
+  const longlong2* desc_b;  // (table offset t0, physical - tier-local segment index)
 };
 
 struct OwnerRef {
   int64_t u;        // table / bucket node id
   int64_t seg_off;  // physical segment index - tier-local segment index
+  int64_t t0;       // table list offset in tab_indices
+  int d;            // table size
+  int32_t tlo;      // first (smallest) table id
+  uint32_t span;    // last - first + 1
 };
 
 __device__ __forceinline__ OwnerRef resolve_owner(const EngineArgs& a, int64_t x) {
-  int64_t o = x, off = 0;
-  if (a.tier_owner) {
-    o = __ldg(&a.tier_owner[x]);
-    off = __ldg(&a.phys_row[o]) - __ldg(&a.row_indptr[x]);
+  const int4 da = __ldg(&a.desc_a[x]);
+  const longlong2 db = __ldg(&a.desc_b[x]);
+  return OwnerRef{da.x, db.y, db.x, da.y, da.z, (uint32_t)da.w};
+}
+
+// Descriptor of tier-local owner x (see EngineArgs::desc_a).
+__global__ void k_owner_desc(const int32_t* __restrict__ own, const int64_t* __restrict__ vrow,
+                             const int64_t* __restrict__ phys_row, const int32_t* __restrict__ owner_map,
+                             const int64_t* __restrict__ tab_indptr, const int32_t* __restrict__ tab_indices,
+                             int64_t cnt, int4* desc_a, longlong2* desc_b) {
+  GRID_STRIDE(x, cnt) {
+    const int64_t o = own[x];
+    const int64_t u = owner_map ? (int64_t)owner_map[o] : o;
+    const int64_t t0 = tab_indptr[u], d = tab_indptr[u + 1] - t0;
+    const int32_t tlo = d ? tab_indices[t0] : 0;
+    const uint32_t span = d ? (uint32_t)(tab_indices[t0 + d - 1] - tlo) + 1u : 0u;
+    desc_a[x] = make_int4((int)u, (int)d, tlo, (int)span);
+    desc_b[x] = make_longlong2(t0, phys_row[o] - vrow[x]);
   }
-  return OwnerRef{a.owner_map ? (int64_t)__ldg(&a.owner_map[o]) : o, off};
 }
 
 // Runtime tier caps (tc_set_tuning; tests lower them to force every tier).
@@ -549,14 +572,11 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       r = rb;
       const OwnerRef ow = resolve_owner(a, x);
       const int64_t u = ow.u;
-      const int64_t t0 = __ldg(&a.tab_indptr[u]);
-      const int64_t d64 = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d64 <= a.d_lo || d64 > a.d_hi) continue;
-      const int d = (int)d64;  // <= the tier cap
+      const int d = ow.d;  // in (d_lo, d_hi]: the list holds this tier's owners only
       acc.to_bucket(a, u, lane);
-      const int32_t* gtab = a.tab_indices + t0;
-      const int32_t tlo = __ldg(&gtab[0]);
-      const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
+      const int32_t* gtab = a.tab_indices + ow.t0;
+      const int32_t tlo = ow.tlo;
+      const uint32_t span = ow.span;
       if (span < (32u << kLw)) {
         // Narrow id span (hub owners at the top of the degree order): the
         // filter words become an exact direct-mapped bitmap over [tlo, tlo+span).
@@ -646,11 +666,9 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
       r = rb;
       const OwnerRef ow = resolve_owner(a, x);
       const int64_t u = ow.u;
-      const int64_t t0 = __ldg(&a.tab_indptr[u]);
-      const int64_t d = __ldg(&a.tab_indptr[u + 1]) - t0;
-      if (d <= a.d_lo) continue;
+      const int64_t d = ow.d;
       acc.to_bucket(a, u, lane);
-      const int32_t* gtab = a.tab_indices + t0;
+      const int32_t* gtab = a.tab_indices + ow.t0;
       const int lb = tab_lb(d);
       if (d <= a.big_cap) {
         if (staged != u) {
@@ -662,8 +680,8 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
           } else {
             for (int i = threadIdx.x; i < staged_d; i += kBigThreads) filt_clear<kLwBig>(bm, __ldg(&staged_list[i]));
           }
-          const int32_t tlo = __ldg(&gtab[0]);
-          const uint32_t span = (uint32_t)(__ldg(&gtab[d - 1]) - tlo) + 1u;
+          const int32_t tlo = ow.tlo;
+          const uint32_t span = ow.span;
           const bool exact = span < (32u << kLwBig);
           if (!exact)
             for (int i = threadIdx.x; i < (1 << lb); i += kBigThreads) bkt[i] = make_int4(kEmpty, kEmpty, kEmpty, kEmpty);
@@ -816,7 +834,10 @@ static long long g_engine_launches = 0;
 #ifndef TCB_MID_WINDOWS
 #define TCB_MID_WINDOWS 2
 #endif
-#define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin, false>
+#ifndef TCB_SMALL_PIPE
+#define TCB_SMALL_PIPE 0
+#endif
+#define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin, TCB_SMALL_PIPE>
 #ifndef TCB_MID_MINB
 #define TCB_MID_MINB 6
 #endif
@@ -1068,8 +1089,14 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
     check_launch();
     const int64_t lo = k == 0 ? 0 : (k == 1 ? c0 : c1);
     const int64_t hi = k == 0 ? c0 : (k == 1 ? c1 : INT64_MAX);
+    int4* desc_a = al.template alloc<int4>((int64_t)L.hsz[k]);
+    longlong2* desc_b = al.template alloc<longlong2>((int64_t)L.hsz[k]);
+    k_owner_desc<<<grid_for((int64_t)L.hsz[k], 256, sm_count() * 8), 256, 0, s>>>(
+        own, vrow, row_indptr, owner_map, tab_indptr, tab_indices, (int64_t)L.hsz[k], desc_a, desc_b);
+    check_launch();
     L.args[k] = EngineArgs{vrow, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
-                           bucket_bounds, nbuckets, nullptr, nx, owner_map, lo, hi, g_big_cap, own, row_indptr};
+                           bucket_bounds, nbuckets, nullptr, nx, owner_map, lo, hi, g_big_cap, own, row_indptr,
+                           desc_a, desc_b};
     L.queue[k] = ctl + 1;
   }
   return L;
