@@ -1,0 +1,48 @@
+"""The NCCL plumbing of the multi-GPU schemes (distributed.py) on one GPU:
+a world-size-1 NCCL process group runs every collective the N-GPU path
+issues (all_to_all_single of counts, lists and ids; all_reduce of the
+uint64-as-int64 partials) on device tensors.  Rank interplay at N > 1 is
+covered by the gloo tests (test_dist_gloo.py) and the per-rank emulation
+(test_gpu_parity.py); this checks that the same code drives NCCL."""
+
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+
+import paper_1406_5687_b200 as tcb
+from paper_1406_5687_b200.distributed import count_space_direct_dist, count_space_surrogate_dist
+from paper_1406_5687_b200.graph_io import rmat_edges
+from paper_1406_5687_b200.sequential import count_middle
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_nccl_world1_schemes(nccl_group):
+    assert dist.get_backend() == "nccl"
+    raw = rmat_edges(14, 16, 5)
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=1 << 14, edges=raw)))
+    T = tcb.count_triangles_seq(g)
+    total, met = count_space_surrogate_dist(g)
+    assert total == T and met.triangles == T
+    total, met = count_space_direct_dist(g)
+    assert total == T and met.triangles == T
+    c = count_middle(g, 0, g.n)  # bench.py's replicated step: range count + all_reduce
+    dist.all_reduce(c)
+    assert int(c.item()) == T
