@@ -140,6 +140,7 @@ __global__ void k_pack_pairs(const int32_t* __restrict__ e, int64_t m,
   GRID_STRIDE(i, m) {
     const unsigned long long k = pair_key(e, i, relabel, b);
     keys[i] = k;
+    if (order_flags && e[2 * i] == e[2 * i + 1]) f |= 4u;  // self-loop: one sentinel survives unique
     if (order_flags && i > 0) {
       const unsigned long long p = pair_key(e, i - 1, relabel, b);
       f |= (k < p ? 1u : 0u) | ((k & mask) < (p & mask) ? 2u : 0u);
@@ -437,10 +438,12 @@ K* sort_keys(Scratch& sc, K* a, K* b, int64_t n, int end_bit, cudaStream_t s, in
 // k_pack_pairs: skip the sort, or sort the high half only (stable LSD
 // passes over an already non-decreasing low half change nothing).
 template <class K>
-K* sort_packed(Scratch& sc, K* a, K* bb, int64_t n, int b, const unsigned* order_flags, cudaStream_t s) {
+K* sort_packed(Scratch& sc, K* a, K* bb, int64_t n, int b, const unsigned* order_flags, cudaStream_t s,
+               unsigned* flags_out = nullptr) {
   unsigned f = 0;
   TC_CUDA(cudaMemcpyAsync(&f, order_flags, sizeof(f), cudaMemcpyDeviceToHost, s));
   sync_stream(s);
+  if (flags_out) *flags_out = f;
   if (!(f & 1u)) return a;
   return sort_keys(sc, a, bb, n, 2 * b, s, (f & 2u) ? 0 : b);
 }
@@ -504,8 +507,12 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   TC_CUDA(cudaMemcpyAsync(lf, &minus1, sizeof(int), cudaMemcpyHostToDevice, s));
   k_present<<<grid_for(L1, kBlock, sms * 8), kBlock, 0, s>>>(fp, L1, cnt, lf);
   check_launch();
-  int64_t K = (int64_t)read_scalar(cnt, s);
-  int64_t Lf = read_scalar(lf, s);
+  unsigned long long hk[2] = {0, 0};  // one transfer for K and Lf
+  TC_CUDA(cudaMemcpyAsync(&hk[0], cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaMemcpyAsync(&hk[1], lf, sizeof(int), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);
+  const int64_t K = (int64_t)hk[0];
+  const int64_t Lf = (int64_t)(int32_t)(uint32_t)hk[1];
   if (K == 0) return;  // only self-loops (graph.py:90-91)
   auto* nsel = sc.alloc<long long>(1);
   const int32_t* relabel = nullptr;
@@ -541,7 +548,8 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   TC_CUDA(cudaMemsetAsync(oflags, 0, sizeof(unsigned), s));
   k_pack_pairs<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(edges, m_raw, relabel, b, ka, oflags);
   check_launch();
-  unsigned long long* sorted = sort_packed(sc, ka, kb, m_raw, b, oflags, s);
+  unsigned hflags = 0;
+  unsigned long long* sorted = sort_packed(sc, ka, kb, m_raw, b, oflags, s, &hflags);
   unsigned long long* uniq = (sorted == ka) ? kb : ka;
   {
     size_t tmp = 0;
@@ -550,12 +558,7 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
     TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, uniq, nsel, m_raw, s));
   }
   int64_t m2 = read_scalar(nsel, s);
-  {  // drop the self-loop sentinel (sorted last) if there was one
-    unsigned long long last = 0;
-    TC_CUDA(cudaMemcpyAsync(&last, uniq + m2 - 1, sizeof(last), cudaMemcpyDeviceToHost, s));
-    sync_stream(s);
-    if (last == (2ull << (2 * b - 1)) - 1) --m2;
-  }
+  if (hflags & 4u) --m2;  // drop the self-loop sentinel (sorted last, once after unique)
   k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, b, out_edges);
   check_launch();
   sync_stream(s);
