@@ -374,8 +374,13 @@ __global__ void __launch_bounds__(kThreads) k_sort_rows_block(const int64_t* __r
 // Phase count for a scatter of `bytes` of output: enough phases that each
 // window fits comfortably in L2 (64 MB), when at most 4 do (every phase
 // re-reads the source); otherwise one.
-inline int scatter_phases(int64_t bytes) {
-  const int64_t window = 64ll << 20;
+#ifndef TCB_REV_WINDOW_MB
+#define TCB_REV_WINDOW_MB 200
+#endif
+#ifndef TCB_SCATTER_WINDOW_MB
+#define TCB_SCATTER_WINDOW_MB 64
+#endif
+inline int scatter_phases(int64_t bytes, int64_t window = (int64_t)TCB_SCATTER_WINDOW_MB << 20) {
   const int64_t p = (bytes + window - 1) / window;
   return p <= 4 ? (int)std::max<int64_t>(1, p) : 1;
 }
@@ -684,7 +689,7 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   if (m) {
     int32_t* cursor = sc.alloc<int32_t>(2 * n);
     TC_CUDA(cudaMemsetAsync(cursor, 0, 2 * n * sizeof(int32_t), s));
-    const int nph = scatter_phases(m * 8);
+    const int nph = scatter_phases(m * 8, (int64_t)TCB_REV_WINDOW_MB << 20);
     k_phase_bounds<<<1, 32, 0, s>>>(rev_indptr, n, nph, bounds);
     check_launch();
     for (int ph = 0; ph < nph; ++ph) {
