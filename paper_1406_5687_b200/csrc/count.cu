@@ -44,6 +44,9 @@ namespace tcb {
 #ifndef TCB_MINBLOCKS
 #define TCB_MINBLOCKS 5
 #endif
+#ifndef TCB_PF_NEXT
+#define TCB_PF_NEXT 0
+#endif
 #ifndef TCB_BIG_PIPE
 #define TCB_BIG_PIPE 0
 #endif
@@ -385,10 +388,16 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt,
-                                             int4* segtab) {
+                                             int4* segtab, int64_t pf_end = 0) {
   const unsigned FULL = 0xffffffffu;
   int s = 0, e = 0;
   if (g0 + lane < g1) segs.get(g0 + lane, s, e);
+#if TCB_PF_NEXT
+  // the next group of this owner: fetch its coordinates now, prefetch its
+  // suffixes into L2 once the setup below has hidden that load
+  int s2 = 0, e2 = 0;
+  if (g1 + lane < pf_end) segs.get(g1 + lane, s2, e2);
+#endif
   int len = e - s;
   unsigned nz = __ballot_sync(FULL, len > 0);  // compact non-empty segments to the low lanes
   int nseg = __popc(nz);
@@ -421,6 +430,9 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
     if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
   }
   __syncwarp();
+#if TCB_PF_NEXT
+  for (int c = s2 & ~31; c < e2; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pool + c));
+#endif
   probe_group<kKind, kLw, kCap, kW, kSb, kPipe>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab, sbits,
                                                 total, lane, npos, cnt);
   if (fast) {
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         int npos = 0;
         for (int64_t g = ra; g < rb; g += 32)
           stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                       lane, npos, acc.cnt, segtab);
+                                                       lane, npos, acc.cnt, segtab, rb + ow.seg_off);
         __syncwarp();
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
         __syncwarp();
@@ -611,7 +623,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       int npos = 0;
       for (int64_t g = ra; g < rb; g += 32)
         stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                      lane, npos, acc.cnt, segtab);
+                                                      lane, npos, acc.cnt, segtab, rb + ow.seg_off);
       __syncwarp();
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
       __syncwarp();
