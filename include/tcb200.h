@@ -61,6 +61,19 @@ int tc_trim_pool(void);
 int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges,
                  int64_t* m_host, int64_t* n_host, tc_stream_t stream);
 
+/* normalize from a host edge list (same result as tc_normalize): host_edges
+ * (int32[2*m_raw], pinned for an asynchronous copy) is copied into
+ * dev_edges (int32[2*m_raw] device staging) in chunks on a copy stream while
+ * each landed chunk's min/max, first occurrences and degree histogram run on
+ * `stream`.  deg (nullable, int32[2*m_raw+1]) receives every label's degree;
+ * *deg_valid = 1 when it is the normalized graph's degree array (dense
+ * labels kept, no self-loop or duplicate dropped), for tc_build_graph_deg.
+ * Replaces the H2D copy + graph.normalize of a host list (graph.py:76-103).
+ * Synchronises (returns m, n). */
+int tc_normalize_host(const int32_t* host_edges, int64_t m_raw, int32_t* dev_edges, int32_t* out_edges,
+                      int64_t* m_host, int64_t* n_host, int32_t* deg, int32_t* deg_valid,
+                      tc_stream_t stream);
+
 /* build_graph + _assemble (graph.py:106-153): degree order (ascending
  * (deg, id), graph.py:152) unless `order` (int32[n], order[i] = original id
  * at canonical position i) is given (the _build_graph_input_order hook,
@@ -78,6 +91,15 @@ int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* or
                    int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                    int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
                    int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
+
+/* tc_build_graph in degree order with the degree array given (deg_hint
+ * int32[n], e.g. from tc_normalize_host with *deg_valid): skips the degree
+ * histogram (graph.py:149-151) and its range check -- the edges must be a
+ * normalized list in [0, n). */
+int tc_build_graph_deg(const int32_t* edges, int64_t m, int64_t n, const int32_t* deg_hint,
+                       int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
+                       int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
+                       int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
 
 /* Full CSR (graph.py:125-127) assembled from the forward and reverse CSRs:
  * row u = its neighbours ascending (predecessors, then N^_u).  full_indptr

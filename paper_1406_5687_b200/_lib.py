@@ -27,6 +27,8 @@ _SIGS = {
     "tc_trim_pool": [],
     "tc_normalize": [_vp, _i64, _vp, _pi64, _pi64, _vp],
     "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_build_graph_deg": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_normalize_host": [_vp, _i64, _vp, _vp, _pi64, _pi64, _vp, _vp, _vp],
     "tc_build_full": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],

@@ -63,17 +63,32 @@ __device__ __forceinline__ int warp_run_end(int32_t key, bool valid, int lane, i
 // separately).  Positions count the raw list, self-loops included: the
 // relative order of the remaining pairs -- all the first-seen ranks depend
 // on -- is the same as after graph.py:89 drops them.
-__global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t npairs, uint32_t* fp) {
+// Chunked form (host-input pipeline): pairs [pos0, pos0 + npairs) of the
+// list, labels >= cap (the speculative table size) set *over and are
+// skipped; deg (nullable) also gets the chunk's degree histogram.
+__global__ void k_first_pos(const int32_t* __restrict__ ids, int64_t npairs, uint32_t* fp, int64_t pos0 = 0,
+                            int64_t cap = INT64_MAX, int* over = nullptr, int32_t* deg = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool ov = false;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
     const int2 p = i < npairs ? reinterpret_cast<const int2*>(ids)[i] : make_int2(-1, -1);
-    const bool valid = i < npairs && p.x != p.y;
-    int st = 0;
-    if (warp_run_end(p.x, valid, lane, &st)) atomicMin(&fp[p.x], (uint32_t)(2 * (i - lane + st)));
-    if (warp_run_end(p.y, valid, lane, &st)) atomicMin(&fp[p.y], (uint32_t)(2 * (i - lane + st) + 1));
+    const bool in = i < npairs && (int64_t)p.x < cap && (int64_t)p.y < cap;
+    ov |= i < npairs && !in;
+    const bool valid = in && p.x != p.y;
+    const int64_t pos = 2 * (pos0 + i - lane);
+    int st = 0, c;
+    if ((c = warp_run_end(p.x, valid, lane, &st))) {
+      atomicMin(&fp[p.x], (uint32_t)(pos + 2 * st));
+      if (deg) atomicAdd(&deg[p.x], c);
+    }
+    if ((c = warp_run_end(p.y, valid, lane, &st))) {
+      atomicMin(&fp[p.y], (uint32_t)(pos + 2 * st + 1));
+      if (deg) atomicAdd(&deg[p.y], c);
+    }
   }
+  if (over && __any_sync(0xffffffffu, ov) && lane == 0) atomicOr(over, 1);
 }
 
 // K = number of present labels, Lf = largest present label.
@@ -478,6 +493,9 @@ T read_scalar(const T* d, cudaStream_t s) {
 
 // ---------------------------------------------------------------- normalize
 
+void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int32_t* out_edges,
+                    int64_t* m_host, int64_t* n_host, cudaStream_t s);
+
 void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t* m_host,
                int64_t* n_host, cudaStream_t s) {
   *m_host = 0;
@@ -505,6 +523,14 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   TC_CUDA(cudaMemsetAsync(fp, 0xFF, L1 * sizeof(uint32_t), s));
   k_first_pos<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(edges, m_raw, fp);
   check_launch();
+  normalize_tail(sc, edges, m_raw, fp, L1, out_edges, m_host, n_host, s);
+}
+
+// normalize from the first-occurrence table on: K, the dense check, the
+// first-seen map, packing, sort and unique (graph.py:94-103).
+void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int32_t* out_edges,
+                    int64_t* m_host, int64_t* n_host, cudaStream_t s) {
+  const int sms = sm_count();
   auto* cnt = sc.alloc<unsigned long long>(1);
   int* lf = sc.alloc<int>(1);
   TC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
@@ -571,29 +597,113 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   *n_host = K;  // graph.py:103
 }
 
+
+// Host-input normalize: the raw list is copied from (pinned) host memory in
+// chunks on a copy stream, and each chunk's min/max, first occurrences and
+// degree histogram run on the compute stream as soon as it has landed, so
+// those passes hide under the PCIe transfer.  The first-occurrence and
+// degree tables are sized speculatively for labels < 2 m_raw + 1 (every
+// dense labelling fits: n <= 2m); a larger label sends the call down the
+// device path once the copy is done.  deg (nullable, int32[2 m_raw + 1]) is
+// the degree of every label; *deg_valid says whether it is the normalized
+// graph's degree array (dense labels kept, nothing dropped), which
+// build_graph can then take instead of its own histogram.
+static cudaStream_t copy_stream() {
+  static cudaStream_t cs[64] = {};
+  int dev = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  if (!cs[dev]) TC_CUDA(cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking));
+  return cs[dev];
+}
+
+void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* out_edges, int64_t* m_host,
+                    int64_t* n_host, int32_t* deg, int32_t* deg_valid, cudaStream_t s) {
+  *m_host = 0;
+  *n_host = 0;
+  if (deg_valid) *deg_valid = 0;
+  TC_REQUIRE(m_raw >= 0, TC_EINVAL, "negative edge count");
+  TC_REQUIRE(m_raw < (1ll << 30), TC_EINVAL, "edge list too long for int32 positions (m_raw >= 2^30)");
+  if (m_raw == 0) return;
+  TC_REQUIRE(((uintptr_t)dev & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
+  Scratch sc(s);
+  const int sms = sm_count();
+  const int64_t cap = std::min<int64_t>(2 * m_raw + 1, INT32_MAX);
+  uint32_t* fp = sc.alloc<uint32_t>(cap);
+  int* mm = sc.alloc<int>(3);  // min, max, label >= cap seen
+  static const int init[3] = {INT_MAX, INT_MIN, 0};
+  TC_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  TC_CUDA(cudaMemsetAsync(fp, 0xFF, cap * sizeof(uint32_t), s));
+  if (deg) TC_CUDA(cudaMemsetAsync(deg, 0, cap * sizeof(int32_t), s));
+
+  cudaStream_t cs = copy_stream();
+  constexpr int kMaxChunks = 16;
+  static cudaEvent_t ev[64][kMaxChunks + 1] = {};
+  int d = 0;
+  TC_CUDA(cudaGetDevice(&d));
+  if (!ev[d][0])
+    for (auto& e : ev[d]) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int64_t chunk_min = 1 << 22;  // pairs (32 MB)
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, m_raw / chunk_min));
+  const int64_t per = (m_raw + nch - 1) / nch;
+  TC_CUDA(cudaEventRecord(ev[d][kMaxChunks], s));  // dev is the caller's, ordered on s
+  TC_CUDA(cudaStreamWaitEvent(cs, ev[d][kMaxChunks], 0));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t o = c * per, mc = std::min(per, m_raw - o);
+    if (mc <= 0) break;
+    TC_CUDA(cudaMemcpyAsync(dev + 2 * o, host + 2 * o, mc * 2 * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+    TC_CUDA(cudaEventRecord(ev[d][c], cs));
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int64_t o = c * per, mc = std::min(per, m_raw - o);
+    if (mc <= 0) break;
+    TC_CUDA(cudaStreamWaitEvent(s, ev[d][c], 0));
+    k_minmax<<<grid_for(2 * mc, kBlock, sms * 8), kBlock, 0, s>>>(dev + 2 * o, 2 * mc, mm, mm + 1);
+    check_launch();
+    k_first_pos<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, fp, o, cap, mm + 2, deg);
+    check_launch();
+  }
+  int hmm[3];
+  TC_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
+  sync_stream(s);
+  TC_REQUIRE(hmm[0] >= 0, TC_EINVAL, "negative node id in edge list");  // graph.py:87-88
+  if (hmm[2]) {  // a label beyond the speculative tables: the device path on the copied list
+    normalize(dev, m_raw, out_edges, m_host, n_host, s);
+    return;
+  }
+  const int64_t L1 = (int64_t)hmm[1] + 1;
+  normalize_tail(sc, dev, m_raw, fp, L1, out_edges, m_host, n_host, s);
+  if (deg_valid) *deg_valid = (*m_host == m_raw && *n_host == L1) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------- build
 
 void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                  int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel, int32_t* orig_ids,
                  int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr, int32_t* rev_seg,
-                 int64_t* rev_cost, cudaStream_t s) {
+                 int64_t* rev_cost, cudaStream_t s, const int32_t* deg_hint = nullptr) {
   TC_REQUIRE(n >= 0 && m >= 0, TC_EINVAL, "negative size");
   TC_REQUIRE(n < (1ll << 31) - 1, TC_EINVAL, "n must fit int32 ids");
   TC_REQUIRE(m < (1ll << 31) - 1, TC_EINVAL, "m must be < 2^31");
   Scratch sc(s);
   int sms = sm_count();
-  // degrees (graph.py:149-151), with the endpoint range check
-  int32_t* deg_orig = sc.alloc<int32_t>(n);
-  if (n) TC_CUDA(cudaMemsetAsync(deg_orig, 0, n * sizeof(int32_t), s));
-  if (m > 0) {
-    TC_REQUIRE(((uintptr_t)edges & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
-    int* bad = sc.alloc<int>(1);
-    TC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-    k_histogram<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, n, deg_orig, bad);
-    check_launch();
-    int hb = read_scalar(bad, s);
-    TC_REQUIRE(!(hb & 1), TC_EINVAL, "negative node id in edge list");
-    TC_REQUIRE(!(hb & 2), TC_EINDEX, "edge endpoint >= n");
+  // degrees (graph.py:149-151), with the endpoint range check -- or the
+  // degrees normalize_host computed while the list was arriving (its
+  // output is in range by construction)
+  const int32_t* deg_orig = deg_hint;
+  if (!deg_hint) {
+    int32_t* h = sc.alloc<int32_t>(n);
+    if (n) TC_CUDA(cudaMemsetAsync(h, 0, n * sizeof(int32_t), s));
+    if (m > 0) {
+      TC_REQUIRE(((uintptr_t)edges & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
+      int* bad = sc.alloc<int>(1);
+      TC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+      k_histogram<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, n, h, bad);
+      check_launch();
+      int hb = read_scalar(bad, s);
+      TC_REQUIRE(!(hb & 1), TC_EINVAL, "negative node id in edge list");
+      TC_REQUIRE(!(hb & 2), TC_EINDEX, "edge endpoint >= n");
+    }
+    deg_orig = h;
   }
   if (n == 0) {
     TC_CUDA(cudaMemsetAsync(eff_indptr, 0, sizeof(int64_t), s));
@@ -782,6 +892,25 @@ int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* or
   return tcb::guarded([&] {
     tcb::build_graph(edges, m, n, order, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
                      rev_indptr, rev_seg, rev_cost, (cudaStream_t)stream);
+  });
+}
+
+int tc_build_graph_deg(const int32_t* edges, int64_t m, int64_t n, const int32_t* deg_hint,
+                       int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
+                       int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
+                       int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    TC_REQUIRE(deg_hint != nullptr, TC_EINVAL, "NULL deg_hint");
+    tcb::build_graph(edges, m, n, nullptr, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
+                     rev_indptr, rev_seg, rev_cost, (cudaStream_t)stream, deg_hint);
+  });
+}
+
+int tc_normalize_host(const int32_t* host_edges, int64_t m_raw, int32_t* dev_edges, int32_t* out_edges,
+                      int64_t* m_host, int64_t* n_host, int32_t* deg, int32_t* deg_valid, tc_stream_t stream) {
+  return tcb::guarded([&] {
+    tcb::normalize_host(host_edges, m_raw, dev_edges, out_edges, m_host, n_host, deg, deg_valid,
+                        (cudaStream_t)stream);
   });
 }
 

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -60,6 +60,9 @@ class RawGraph:
 
     n: int
     edges: object
+    # degree of every node of a normalized list, when normalize computed it
+    # on the way (host-input pipeline); build_graph then skips its histogram
+    _deg: object = field(default=None, repr=False, compare=False)
 
     @classmethod
     def from_pairs(cls, pairs, n=None):
@@ -188,6 +191,10 @@ def normalize(raw: RawGraph) -> RawGraph:
     list.  Returns a RawGraph whose edges are a sorted (m, 2) int32 device
     tensor."""
     dev = _lib.device()
+    h = raw.edges
+    if (isinstance(h, torch.Tensor) and h.device.type == "cpu" and h.dtype == torch.int32 and h.is_pinned()
+            and h.is_contiguous() and h.numel() >= _HOST_PIPELINE_MIN):
+        return _normalize_host(h.reshape(-1, 2), dev)
     e = _as_device_pairs(raw.edges, dev)
     m_raw = e.shape[0]
     out = torch.empty((max(m_raw, 1), 2), dtype=torch.int32, device=dev)
@@ -196,6 +203,26 @@ def normalize(raw: RawGraph) -> RawGraph:
     _lib.call("tc_normalize", _lib.ptr(e), m_raw, _lib.ptr(out), ctypes.byref(m), ctypes.byref(n),
               _lib.stream())
     return RawGraph(n=int(n.value), edges=out[: m.value])
+
+
+# host lists of at least this many ids take the chunked copy pipeline
+_HOST_PIPELINE_MIN = 1 << 23
+
+
+def _normalize_host(h, dev) -> RawGraph:
+    """normalize of a pinned host int32 list: the H2D copy runs in chunks on a
+    copy stream with each chunk's first-occurrence / degree passes behind it
+    (tc_normalize_host)."""
+    m_raw = h.shape[0]
+    staging = torch.empty((m_raw, 2), dtype=torch.int32, device=dev)
+    out = torch.empty((m_raw, 2), dtype=torch.int32, device=dev)
+    deg = torch.empty(2 * m_raw + 1, dtype=torch.int32, device=dev)
+    m, n, valid = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int32(0)
+    _lib.call("tc_normalize_host", _lib.ptr(h), m_raw, _lib.ptr(staging), _lib.ptr(out), ctypes.byref(m),
+              ctypes.byref(n), _lib.ptr(deg), ctypes.byref(valid), _lib.stream())
+    del staging
+    nv = int(n.value)
+    return RawGraph(n=nv, edges=out[: m.value], _deg=deg[:nv] if valid.value else None)
 
 
 def _assemble(raw: RawGraph, order) -> Graph:
@@ -211,7 +238,9 @@ def _assemble(raw: RawGraph, order) -> Graph:
     order_t = None
     if order is not None:
         order_t = torch.as_tensor(np.asarray(order, dtype=np.int32)).to(dev).contiguous()
-    _lib.call("tc_build_graph", _lib.ptr(e), m, n, _lib.ptr(order_t), _lib.ptr(eff_indptr),
+    hint = raw._deg if (order is None and raw._deg is not None and raw._deg.numel() == n) else None
+    _lib.call("tc_build_graph" if hint is None else "tc_build_graph_deg", _lib.ptr(e), m, n,
+              _lib.ptr(order_t if hint is None else hint), _lib.ptr(eff_indptr),
               _lib.ptr(eff_indices), _lib.ptr(relabel), _lib.ptr(orig_ids), _lib.ptr(deg),
               _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_seg), _lib.ptr(rev_cost), _lib.stream())
     g = Graph(n, m, eff_indptr[: n + 1], eff_indices[:m], relabel[:n], orig_ids[:n], deg[:n],

@@ -388,6 +388,38 @@ def test_build_row_sort_classes():
         assert tcb.count_triangles_seq(g) == O.count_triangles(og)
 
 
+def _host_pinned(a):
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(a, np.int32).reshape(-1, 2))).pin_memory()
+
+
+@pytest.mark.parametrize("case", ["pa", "dups_loops", "sparse_big", "sparse_small"])
+def test_normalize_host_pipeline(case, monkeypatch):
+    """normalize of a pinned host list (chunked H2D copy with the
+    first-occurrence / degree passes behind it) equals the device path; the
+    degree array it hands to build_graph gives the same graph; labels
+    beyond the speculative tables fall back to the device path."""
+    monkeypatch.setattr(G, "_HOST_PIPELINE_MIN", 0)
+    rng = np.random.default_rng(3)
+    if case == "pa":  # dense labels, no self-loop or duplicate: degrees handed over
+        raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy()
+    elif case == "dups_loops":
+        raw = rng.integers(0, 5000, size=(300_000, 2))
+    elif case == "sparse_big":  # labels far above 2 m_raw + 1
+        raw = rng.integers(0, 5000, size=(100_000, 2)) * 100_003
+    else:  # sparse but small labels: first-seen compaction on the pipelined path
+        raw = rng.integers(0, 30_000, size=(40_000, 2)) * 2
+    h = _host_pinned(raw)
+    got = tcb.normalize(tcb.RawGraph(n=0, edges=h))
+    want = tcb.normalize(tcb.RawGraph(n=0, edges=h.cuda()))
+    assert got.n == want.n
+    assert torch.equal(got.edges, want.edges)
+    assert (got._deg is not None) == (case == "pa")
+    g1, g2 = tcb.build_graph(got), tcb.build_graph(want)
+    for f in ("eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg"):
+        assert torch.equal(getattr(g1, f), getattr(g2, f)), f
+    assert tcb.count_triangles_seq(g1) == tcb.count_triangles_seq(g2)
+
+
 @pytest.mark.parametrize("name", ["er_60_0.2_21", "pa_1500_12_3", "sparse_labels", "rmat_s10", "gnm_2000_16000", "k9"])
 def test_multi_rank_path_emulated(name):
     """The per-rank device kernels of the multi-GPU surrogate protocol
