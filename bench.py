@@ -7,7 +7,8 @@ Contract:
 A step of `value` is one count of the whole graph (count_triangles_seq: the
 middle-vertex engine's plan + engine kernels) with the oriented CSR resident
 in HBM; metric = m / step time.  `e2e` is the same metric through the public
-API with host buffers: pinned raw edge list -> H2D -> normalize ->
+API with host buffers: pinned raw edge list -> normalize (which copies it to
+the device in chunks, overlapping its first passes with the copy) ->
 build_graph -> count -> D2H of the count, every step.  The reference arm
 (--impl reference) times the reference's CPU algorithm (the C restatement in
 oracle/, all host threads, the count_dynamic task queue) on a bounded

@@ -181,7 +181,8 @@ int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_
 /* Engine tier caps (testing / tuning): key 0 = small warp-tier table cap
  * (0..256, default 256), key 2 = mid warp-tier cap (0..512, default 512),
  * key 1 = block-tier staged-table cap (0..4096, default 4096; larger tables
- * use binary search in global memory). */
+ * use binary search in global memory), key 3 = pairs per chunk of
+ * tc_normalize_host's copy pipeline (>= 1, default 2^22; at most 16 chunks). */
 int tc_set_tuning(int32_t key, int64_t value);
 
 /* |a ∩ b| of two strictly ascending int32 lists (_kernels.py:15-37). */

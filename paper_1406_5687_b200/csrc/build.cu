@@ -6,12 +6,15 @@
 // CSR builds.  Every sort is stable, which is what makes the outputs
 // bit-identical to numpy's stable lexsort / unique.
 #include <cub/cub.cuh>
+#include <cub/device/device_merge.cuh>
 
 #include "common.cuh"
 
 namespace tcb {
 
 static constexpr uint32_t kInf32 = 0xFFFFFFFFu;
+
+int64_t g_host_chunk = 1 << 22;  // pairs (32 MB)
 static constexpr int kBlock = 256;
 
 // Pull-engine cost model (count.cu reads it through rev_cost): per
@@ -493,8 +496,10 @@ T read_scalar(const T* d, cudaStream_t s) {
 
 // ---------------------------------------------------------------- normalize
 
-void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int32_t* out_edges,
-                    int64_t* m_host, int64_t* n_host, cudaStream_t s);
+void present_labels(Scratch& sc, const uint32_t* fp, int64_t L1, int64_t* K, int64_t* Lf, cudaStream_t s);
+void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int64_t K,
+                    int64_t Lf, int32_t* out_edges, int64_t* m_host, int64_t* n_host, cudaStream_t s,
+                    const unsigned long long* sorted32 = nullptr, bool sentinel = false);
 
 void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t* m_host,
                int64_t* n_host, cudaStream_t s) {
@@ -523,13 +528,13 @@ void normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_t*
   TC_CUDA(cudaMemsetAsync(fp, 0xFF, L1 * sizeof(uint32_t), s));
   k_first_pos<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(edges, m_raw, fp);
   check_launch();
-  normalize_tail(sc, edges, m_raw, fp, L1, out_edges, m_host, n_host, s);
+  int64_t K = 0, Lf = 0;
+  present_labels(sc, fp, L1, &K, &Lf, s);
+  normalize_tail(sc, edges, m_raw, fp, L1, K, Lf, out_edges, m_host, n_host, s);
 }
 
-// normalize from the first-occurrence table on: K, the dense check, the
-// first-seen map, packing, sort and unique (graph.py:94-103).
-void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int32_t* out_edges,
-                    int64_t* m_host, int64_t* n_host, cudaStream_t s) {
+// K = labels present outside self-loops, Lf = the largest (graph.py:92-94).
+void present_labels(Scratch& sc, const uint32_t* fp, int64_t L1, int64_t* K, int64_t* Lf, cudaStream_t s) {
   const int sms = sm_count();
   auto* cnt = sc.alloc<unsigned long long>(1);
   int* lf = sc.alloc<int>(1);
@@ -542,11 +547,36 @@ void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* 
   TC_CUDA(cudaMemcpyAsync(&hk[0], cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   TC_CUDA(cudaMemcpyAsync(&hk[1], lf, sizeof(int), cudaMemcpyDeviceToHost, s));
   sync_stream(s);
-  const int64_t K = (int64_t)hk[0];
-  const int64_t Lf = (int64_t)(int32_t)(uint32_t)hk[1];
+  *K = (int64_t)hk[0];
+  *Lf = (int64_t)(int32_t)(uint32_t)hk[1];
+}
+
+// normalize from the label census on: the first-seen map, packing, sort
+// and unique (graph.py:95-103).  sorted32 (nullable): the list's keys
+// (min << 32 | max, raw labels; a self-loop as ~0, flagged by `sentinel`)
+// already sorted -- used when the labels are dense, so only the unique
+// pass remains.
+void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* fp, int64_t L1, int64_t K,
+                    int64_t Lf, int32_t* out_edges, int64_t* m_host, int64_t* n_host, cudaStream_t s,
+                    const unsigned long long* sorted32, bool sentinel) {
+  const int sms = sm_count();
   if (K == 0) return;  // only self-loops (graph.py:90-91)
   auto* nsel = sc.alloc<long long>(1);
   const int32_t* relabel = nullptr;
+  if (sorted32 && K == Lf + 1) {  // dense labels kept: unique + unpack of the presorted keys
+    unsigned long long* uniq = sc.alloc<unsigned long long>(m_raw);
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted32, uniq, nsel, m_raw, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted32, uniq, nsel, m_raw, s));
+    const int64_t m2 = read_scalar(nsel, s) - (sentinel ? 1 : 0);  // the self-loop key sorts last
+    k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, 32, out_edges);
+    check_launch();
+    sync_stream(s);
+    *m_host = m2;
+    *n_host = K;
+    return;
+  }
 
   if (K != Lf + 1) {
     // first-seen compaction (graph.py:96-98): new id = rank of first position
@@ -608,6 +638,10 @@ void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* 
 // the degree of every label; *deg_valid says whether it is the normalized
 // graph's degree array (dense labels kept, nothing dropped), which
 // build_graph can then take instead of its own histogram.
+struct KeyLess {
+  __device__ bool operator()(unsigned long long a, unsigned long long b) const { return a < b; }
+};
+
 static cudaStream_t copy_stream() {
   static cudaStream_t cs[64] = {};
   int dev = 0;
@@ -642,8 +676,7 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   TC_CUDA(cudaGetDevice(&d));
   if (!ev[d][0])
     for (auto& e : ev[d]) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  const int64_t chunk_min = 1 << 22;  // pairs (32 MB)
-  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, m_raw / chunk_min));
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, m_raw / g_host_chunk));
   const int64_t per = (m_raw + nch - 1) / nch;
   TC_CUDA(cudaEventRecord(ev[d][kMaxChunks], s));  // dev is the caller's, ordered on s
   TC_CUDA(cudaStreamWaitEvent(cs, ev[d][kMaxChunks], 0));
@@ -653,6 +686,19 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
     TC_CUDA(cudaMemcpyAsync(dev + 2 * o, host + 2 * o, mc * 2 * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
     TC_CUDA(cudaEventRecord(ev[d][c], cs));
   }
+  // Behind the copy, each chunk's keys (min << 32 | max, raw labels) are
+  // packed and sorted -- by the smaller endpoint only (stable) when the
+  // chunk is already ordered by its larger one, as a generator emitting
+  // edges per new node is -- so the chunks become sorted runs that a merge
+  // tree joins after the copy, instead of a full radix sort then.
+  unsigned long long* ka = sc.alloc<unsigned long long>(m_raw);
+  unsigned long long* kb = sc.alloc<unsigned long long>(m_raw);
+  unsigned* cflags = sc.alloc<unsigned>(kMaxChunks);
+  TC_CUDA(cudaMemsetAsync(cflags, 0, kMaxChunks * sizeof(unsigned), s));
+  size_t sort_tmp = 0;
+  TC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, ka, kb, per, 0, 64, s));
+  void* sort_ws = sc.bytes(sort_tmp);
+  bool runs = true, any_loop = false;
   for (int c = 0; c < nch; ++c) {
     const int64_t o = c * per, mc = std::min(per, m_raw - o);
     if (mc <= 0) break;
@@ -661,6 +707,27 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
     check_launch();
     k_first_pos<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, fp, o, cap, mm + 2, deg);
     check_launch();
+    if (!runs) continue;
+    k_pack_pairs<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, nullptr, 32, ka + o,
+                                                                     cflags + c);
+    check_launch();
+    unsigned hf[2] = {0, 0};  // (chunk flags, largest label so far); the copy stream runs on meanwhile
+    TC_CUDA(cudaMemcpyAsync(&hf[0], cflags + c, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&hf[1], mm + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    sync_stream(s);
+    if ((int)hf[1] < 0) {
+      runs = false;
+      continue;
+    }
+    any_loop |= (hf[0] & 4u) != 0;  // a self-loop packs as ~0: sorts last, one survives unique
+    const int hi_bits = 32 + std::max(1, bits_for((uint64_t)hf[1]));
+    size_t tb = sort_tmp;
+    if (!(hf[0] & 1u))  // already sorted
+      TC_CUDA(cudaMemcpyAsync(kb + o, ka + o, mc * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    else if (!(hf[0] & 2u))  // larger endpoints non-decreasing: a stable sort by the smaller one suffices
+      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 32, hi_bits, s));
+    else  // (e.g. a generator's seed clique) the whole key
+      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 0, hi_bits, s));
   }
   int hmm[3];
   TC_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
@@ -671,7 +738,42 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
     return;
   }
   const int64_t L1 = (int64_t)hmm[1] + 1;
-  normalize_tail(sc, dev, m_raw, fp, L1, out_edges, m_host, n_host, s);
+  int64_t K = 0, Lf = 0;
+  present_labels(sc, fp, L1, &K, &Lf, s);
+  const unsigned long long* sorted32 = nullptr;
+  if (runs && K == Lf + 1) {  // merge tree over the sorted chunk runs (kb -> ka -> ...)
+    std::vector<std::pair<int64_t, int64_t>> rr;
+    for (int c = 0; c < nch; ++c)
+      if (c * per < m_raw) rr.emplace_back(c * per, std::min(per, m_raw - c * per));
+    unsigned long long *src = kb, *dst = ka;
+    size_t mcap = 0;
+    void* mws = nullptr;
+    while (rr.size() > 1) {
+      std::vector<std::pair<int64_t, int64_t>> nr;
+      for (size_t i = 0; i < rr.size(); i += 2) {
+        const int64_t o = rr[i].first, l1 = rr[i].second;
+        if (i + 1 == rr.size()) {
+          TC_CUDA(cudaMemcpyAsync(dst + o, src + o, l1 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+          nr.emplace_back(o, l1);
+          continue;
+        }
+        const int64_t l2 = rr[i + 1].second;
+        size_t need = 0;
+        TC_CUDA(cub::DeviceMerge::MergeKeys(nullptr, need, src + o, (int)l1, src + o + l1, (int)l2, dst + o,
+                                            KeyLess(), s));
+        if (need > mcap) {
+          mws = sc.bytes(need);
+          mcap = need;
+        }
+        TC_CUDA(cub::DeviceMerge::MergeKeys(mws, need, src + o, (int)l1, src + o + l1, (int)l2, dst + o, KeyLess(), s));
+        nr.emplace_back(o, l1 + l2);
+      }
+      rr.swap(nr);
+      std::swap(src, dst);
+    }
+    sorted32 = src;
+  }
+  normalize_tail(sc, dev, m_raw, fp, L1, K, Lf, out_edges, m_host, n_host, s, sorted32, any_loop);
   if (deg_valid) *deg_valid = (*m_host == m_raw && *n_host == L1) ? 1 : 0;
 }
 

@@ -98,6 +98,9 @@ inline void sync_stream(cudaStream_t s) { TC_CUDA(cudaStreamSynchronize(s)); }
 // check_launch); CUB's kernels are not counted.  Read by tc_launch_count.
 extern unsigned long long g_launches;
 
+// Pairs per chunk of the host-input normalize pipeline (tc_set_tuning key 3).
+extern int64_t g_host_chunk;
+
 inline void check_launch() {
   ++g_launches;
   TC_CUDA(cudaGetLastError());

@@ -1398,6 +1398,9 @@ int tc_set_tuning(int32_t key, int64_t value) {
     } else if (key == 1) {
       TC_REQUIRE(value >= 0 && value <= tcb::kBigCap, TC_EINVAL, "block cap out of range");
       tcb::g_big_cap = (int)value;
+    } else if (key == 3) {
+      TC_REQUIRE(value >= 1, TC_EINVAL, "host chunk size out of range");
+      tcb::g_host_chunk = value;
     } else {
       throw tcb::Error(TC_EINVAL, "unknown tuning key");
     }

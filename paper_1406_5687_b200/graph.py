@@ -206,7 +206,7 @@ def normalize(raw: RawGraph) -> RawGraph:
 
 
 # host lists of at least this many ids take the chunked copy pipeline
-_HOST_PIPELINE_MIN = 1 << 23
+_HOST_PIPELINE_MIN = int(os.environ.get("TCB_HOST_PIPELINE_MIN", 1 << 23))
 
 
 def _normalize_host(h, dev) -> RawGraph:

@@ -392,16 +392,25 @@ def _host_pinned(a):
     return torch.as_tensor(np.ascontiguousarray(np.asarray(a, np.int32).reshape(-1, 2))).pin_memory()
 
 
-@pytest.mark.parametrize("case", ["pa", "dups_loops", "sparse_big", "sparse_small"])
-def test_normalize_host_pipeline(case, monkeypatch):
+@pytest.mark.parametrize("chunk", [1 << 22, 100_000])
+@pytest.mark.parametrize("case", ["pa", "pa_sparse", "sorted", "dups_loops", "sparse_big", "sparse_small"])
+def test_normalize_host_pipeline(case, chunk, monkeypatch):
     """normalize of a pinned host list (chunked H2D copy with the
-    first-occurrence / degree passes behind it) equals the device path; the
-    degree array it hands to build_graph gives the same graph; labels
-    beyond the speculative tables fall back to the device path."""
+    first-occurrence / degree passes and per-chunk sorted runs behind it,
+    merge tree after) equals the device path; the degree array it hands to
+    build_graph gives the same graph; labels beyond the speculative tables
+    fall back to the device path."""
     monkeypatch.setattr(G, "_HOST_PIPELINE_MIN", 0)
+    from paper_1406_5687_b200 import _lib
+    L = _lib.lib()
+    assert L.tc_set_tuning(3, chunk) == 0
     rng = np.random.default_rng(3)
     if case == "pa":  # dense labels, no self-loop or duplicate: degrees handed over
         raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy()
+    elif case == "pa_sparse":  # per-chunk runs, but labels not dense: first-seen map
+        raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy() * 2
+    elif case == "sorted":  # an already normalized list
+        raw = tcb.normalize(tcb.RawGraph.from_pairs(rng.integers(0, 30000, size=(300_000, 2)))).edges.cpu().numpy()
     elif case == "dups_loops":
         raw = rng.integers(0, 5000, size=(300_000, 2))
     elif case == "sparse_big":  # labels far above 2 m_raw + 1
@@ -413,11 +422,12 @@ def test_normalize_host_pipeline(case, monkeypatch):
     want = tcb.normalize(tcb.RawGraph(n=0, edges=h.cuda()))
     assert got.n == want.n
     assert torch.equal(got.edges, want.edges)
-    assert (got._deg is not None) == (case == "pa")
+    assert (got._deg is not None) == (case in ("pa", "sorted"))
     g1, g2 = tcb.build_graph(got), tcb.build_graph(want)
     for f in ("eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg"):
         assert torch.equal(getattr(g1, f), getattr(g2, f)), f
     assert tcb.count_triangles_seq(g1) == tcb.count_triangles_seq(g2)
+    assert L.tc_set_tuning(3, 1 << 22) == 0
 
 
 @pytest.mark.parametrize("name", ["er_60_0.2_21", "pa_1500_12_3", "sparse_labels", "rmat_s10", "gnm_2000_16000", "k9"])
