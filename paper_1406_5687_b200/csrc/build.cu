@@ -690,15 +690,46 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   // packed and sorted -- by the smaller endpoint only (stable) when the
   // chunk is already ordered by its larger one, as a generator emitting
   // edges per new node is -- so the chunks become sorted runs that a merge
-  // tree joins after the copy, instead of a full radix sort then.
+  // tree joins, mostly while the copy is still running, instead of a full
+  // radix sort after it.
   unsigned long long* ka = sc.alloc<unsigned long long>(m_raw);
   unsigned long long* kb = sc.alloc<unsigned long long>(m_raw);
+  unsigned long long* kc = sc.alloc<unsigned long long>(m_raw);
   unsigned* cflags = sc.alloc<unsigned>(kMaxChunks);
   TC_CUDA(cudaMemsetAsync(cflags, 0, kMaxChunks * sizeof(unsigned), s));
   size_t sort_tmp = 0;
   TC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, ka, kb, per, 0, 64, s));
   void* sort_ws = sc.bytes(sort_tmp);
   bool runs = true, any_loop = false;
+  // Sorted runs as a binary counter: a run of level l holds 2^l chunks; two
+  // runs of equal level merge while later chunks are still being copied.
+  // A merge writes a third buffer (its region is free in every buffer but
+  // the two it reads), so runs may live in any of ka / kb / kc.
+  struct Run {
+    int64_t o, len;
+    unsigned long long* buf;
+    int level;
+  };
+  std::vector<Run> stack;
+  size_t mcap = 0;
+  void* mws = nullptr;
+  auto merge_top = [&]() {
+    const Run r2 = stack.back();
+    stack.pop_back();
+    const Run r1 = stack.back();
+    stack.pop_back();
+    unsigned long long* z = (r1.buf != ka && r2.buf != ka) ? ka : (r1.buf != kb && r2.buf != kb) ? kb : kc;
+    size_t need = 0;
+    TC_CUDA(cub::DeviceMerge::MergeKeys(nullptr, need, r1.buf + r1.o, (int)r1.len, r2.buf + r2.o, (int)r2.len,
+                                        z + r1.o, KeyLess(), s));
+    if (need > mcap) {
+      mws = sc.bytes(need);
+      mcap = need;
+    }
+    TC_CUDA(cub::DeviceMerge::MergeKeys(mws, need, r1.buf + r1.o, (int)r1.len, r2.buf + r2.o, (int)r2.len, z + r1.o,
+                                        KeyLess(), s));
+    stack.push_back(Run{r1.o, r1.len + r2.len, z, std::max(r1.level, r2.level) + 1});
+  };
   for (int c = 0; c < nch; ++c) {
     const int64_t o = c * per, mc = std::min(per, m_raw - o);
     if (mc <= 0) break;
@@ -728,6 +759,8 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
       TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 32, hi_bits, s));
     else  // (e.g. a generator's seed clique) the whole key
       TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 0, hi_bits, s));
+    stack.push_back(Run{o, mc, kb, 0});
+    while (stack.size() >= 2 && stack[stack.size() - 1].level == stack[stack.size() - 2].level) merge_top();
   }
   int hmm[3];
   TC_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
@@ -741,37 +774,9 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   int64_t K = 0, Lf = 0;
   present_labels(sc, fp, L1, &K, &Lf, s);
   const unsigned long long* sorted32 = nullptr;
-  if (runs && K == Lf + 1) {  // merge tree over the sorted chunk runs (kb -> ka -> ...)
-    std::vector<std::pair<int64_t, int64_t>> rr;
-    for (int c = 0; c < nch; ++c)
-      if (c * per < m_raw) rr.emplace_back(c * per, std::min(per, m_raw - c * per));
-    unsigned long long *src = kb, *dst = ka;
-    size_t mcap = 0;
-    void* mws = nullptr;
-    while (rr.size() > 1) {
-      std::vector<std::pair<int64_t, int64_t>> nr;
-      for (size_t i = 0; i < rr.size(); i += 2) {
-        const int64_t o = rr[i].first, l1 = rr[i].second;
-        if (i + 1 == rr.size()) {
-          TC_CUDA(cudaMemcpyAsync(dst + o, src + o, l1 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-          nr.emplace_back(o, l1);
-          continue;
-        }
-        const int64_t l2 = rr[i + 1].second;
-        size_t need = 0;
-        TC_CUDA(cub::DeviceMerge::MergeKeys(nullptr, need, src + o, (int)l1, src + o + l1, (int)l2, dst + o,
-                                            KeyLess(), s));
-        if (need > mcap) {
-          mws = sc.bytes(need);
-          mcap = need;
-        }
-        TC_CUDA(cub::DeviceMerge::MergeKeys(mws, need, src + o, (int)l1, src + o + l1, (int)l2, dst + o, KeyLess(), s));
-        nr.emplace_back(o, l1 + l2);
-      }
-      rr.swap(nr);
-      std::swap(src, dst);
-    }
-    sorted32 = src;
+  if (runs && K == Lf + 1) {  // join the remaining runs, smallest first
+    while (stack.size() > 1) merge_top();
+    sorted32 = stack[0].buf;
   }
   normalize_tail(sc, dev, m_raw, fp, L1, K, Lf, out_edges, m_host, n_host, s, sorted32, any_loop);
   if (deg_valid) *deg_valid = (*m_host == m_raw && *n_host == L1) ? 1 : 0;
