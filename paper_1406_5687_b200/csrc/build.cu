@@ -7,6 +7,7 @@
 // bit-identical to numpy's stable lexsort / unique.
 #include <cub/cub.cuh>
 #include <cub/device/device_merge.cuh>
+#include <thrust/iterator/transform_output_iterator.h>
 
 #include "common.cuh"
 
@@ -169,15 +170,14 @@ __global__ void k_pack_pairs(const int32_t* __restrict__ e, int64_t m,
   if ((threadIdx.x & 31) == 0 && f) atomicOr(order_flags, f);
 }
 
-__global__ void k_unpack_pairs(const unsigned long long* __restrict__ keys, int64_t m, int b,
-                               int32_t* out) {
-  unsigned long long mask = (1ull << b) - 1;
-  GRID_STRIDE(i, m) {
-    unsigned long long k = keys[i];
-    out[2 * i] = (int32_t)(k >> b);
-    out[2 * i + 1] = (int32_t)(k & mask);
+// (lo << b | hi) key -> (lo, hi) pair, written by the unique pass itself.
+struct UnpackKey {
+  int b;
+  __host__ __device__ int2 operator()(unsigned long long k) const {
+    return make_int2((int32_t)(k >> b), (int32_t)(k & ((1ull << b) - 1)));
   }
-}
+};
+
 
 // Degree histogram over the pair list (thread per pair, run-aggregated),
 // fused with the endpoint range check: out-of-range ids set `bad` (bit 0
@@ -563,16 +563,13 @@ void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* 
   if (K == 0) return;  // only self-loops (graph.py:90-91)
   auto* nsel = sc.alloc<long long>(1);
   const int32_t* relabel = nullptr;
-  if (sorted32 && K == Lf + 1) {  // dense labels kept: unique + unpack of the presorted keys
-    unsigned long long* uniq = sc.alloc<unsigned long long>(m_raw);
+  if (sorted32 && K == Lf + 1) {  // dense labels kept: unique (writing pairs) of the presorted keys
+    auto out = thrust::make_transform_output_iterator(reinterpret_cast<int2*>(out_edges), UnpackKey{32});
     size_t tmp = 0;
-    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted32, uniq, nsel, m_raw, s));
+    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted32, out, nsel, m_raw, s));
     void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted32, uniq, nsel, m_raw, s));
+    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted32, out, nsel, m_raw, s));
     const int64_t m2 = read_scalar(nsel, s) - (sentinel ? 1 : 0);  // the self-loop key sorts last
-    k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, 32, out_edges);
-    check_launch();
-    sync_stream(s);
     *m_host = m2;
     *n_host = K;
     return;
@@ -611,18 +608,15 @@ void normalize_tail(Scratch& sc, const int32_t* edges, int64_t m_raw, uint32_t* 
   check_launch();
   unsigned hflags = 0;
   unsigned long long* sorted = sort_packed(sc, ka, kb, m_raw, b, oflags, s, &hflags);
-  unsigned long long* uniq = (sorted == ka) ? kb : ka;
   {
+    auto out = thrust::make_transform_output_iterator(reinterpret_cast<int2*>(out_edges), UnpackKey{b});
     size_t tmp = 0;
-    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, uniq, nsel, m_raw, s));
+    TC_CUDA(cub::DeviceSelect::Unique(nullptr, tmp, sorted, out, nsel, m_raw, s));
     void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, uniq, nsel, m_raw, s));
+    TC_CUDA(cub::DeviceSelect::Unique(t, tmp, sorted, out, nsel, m_raw, s));
   }
   int64_t m2 = read_scalar(nsel, s);
   if (hflags & 4u) --m2;  // drop the self-loop sentinel (sorted last, once after unique)
-  k_unpack_pairs<<<grid_for(m2, kBlock, sms * 16), kBlock, 0, s>>>(uniq, m2, b, out_edges);
-  check_launch();
-  sync_stream(s);
   *m_host = m2;
   *n_host = K;  // graph.py:103
 }
