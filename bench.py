@@ -14,10 +14,10 @@ build_graph -> count -> D2H of the count, every step.  The reference arm
 oracle/, all host threads, the count_dynamic task queue) on a bounded
 sample of the same workload.
 
-N > 1 (torchrun, one rank per GPU): every rank builds the graph, owns a
-contiguous middle-vertex range balanced by the engine's cost prefix and the
-per-GPU uint64 counts are combined with an NCCL all-reduce inside the timed
-region; timing is the max over ranks ("strong" scaling: total work fixed).
+N > 1 (torchrun, one rank per GPU): every rank builds the graph, runs the
+chunks c = rank (mod N) of the engine's plan (cut for the workers of all N
+GPUs, every tier split; count_middle_part) and the per-GPU uint64 counts
+are combined with an NCCL all-reduce inside the timed region; timing is the max over ranks ("strong" scaling: total work fixed).
 --mode surrogate / direct run the paper's space-efficient schemes instead
 (node-range shards, N^ lists exchanged with NCCL all-to-all, then the
 all-reduce; distributed.py).
@@ -249,7 +249,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
     ap.add_argument("--mode", default="replicated", choices=["replicated", "surrogate", "direct"],
-                    help="N>1: replicated graph with cost-balanced middle-vertex ranges (default), the paper's "
+                    help="N>1: replicated graph, the engine's chunk plan interleaved across ranks (default), the paper's "
                          "non-overlapping partition with surrogate list exchange, or the direct scheme as a "
                          "deduplicated pull")
     args = ap.parse_args()
@@ -276,8 +276,7 @@ def _gpu_arm_core(args):
 
     import paper_1406_5687_b200 as tcb
     from paper_1406_5687_b200 import _lib
-    from paper_1406_5687_b200.partitioning import balanced_bounds
-    from paper_1406_5687_b200.sequential import count_middle
+    from paper_1406_5687_b200.sequential import count_middle, count_middle_part
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -312,12 +311,6 @@ def _gpu_arm_core(args):
     W = int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum())
 
     mode = args.mode if world > 1 else "single"
-    if mode == "replicated":
-        ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
-        ub = balanced_bounds(ucost, 0, n, world).cpu().numpy()
-        u0, u1 = int(ub[rank]), int(ub[rank + 1])
-    else:
-        u0, u1 = 0, n
     out = torch.empty(1, dtype=torch.int64, device=dev)
     if mode in ("surrogate", "direct"):
         from paper_1406_5687_b200.distributed import direct_rank, shard_of, surrogate_rank
@@ -335,9 +328,11 @@ def _gpu_arm_core(args):
             total, _ = rank_fn(shard, sb)
             out.fill_(total)
             return out
-        count_middle(g, u0, u1, out=out)
-        if world > 1:
+        if world > 1:  # replicated: this rank's interleaved share of the engine's chunks
+            count_middle_part(g, rank, world, out=out)
             dist.all_reduce(out)
+        else:
+            count_middle(g, out=out)
         return out
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -392,7 +387,7 @@ def _gpu_arm_core(args):
             if mode in ("surrogate", "direct"):
                 tri, _ = rank_fn(shard_of(gg, int(sb[rank]), int(sb[rank + 1])), sb)
             elif world > 1:
-                c = count_middle(gg, u0, u1)
+                c = count_middle_part(gg, rank, world)
                 dist.all_reduce(c)
                 tri = int(c.item())
             else:
@@ -435,7 +430,7 @@ def _gpu_arm_core(args):
                    "triangles": T, "W_succsum": W,
                    "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
                    "parallelism": {"single": "1 GPU",
-                                   "replicated": f"{world} GPUs, replicated graph, cost-balanced middle-vertex ranges + NCCL all-reduce",
+                                   "replicated": f"{world} GPUs, replicated graph, engine chunks interleaved across ranks + NCCL all-reduce",
                                    "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
                                                 "(NCCL all-to-all) + NCCL all-reduce",
                                    "direct": f"{world} GPUs, SUCC_SUM node-range shards, deduplicated pull of remote "

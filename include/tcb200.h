@@ -138,6 +138,19 @@ int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const 
 int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream);
 int tc_plan_free(tc_plan_t plan);
 
+/* Interleaved split of one plan across `nparts` devices that each hold the
+ * whole graph (the replicated multi-GPU count; the work split of
+ * dynamic_lb.py:68-109 across ranks instead of one rank's workers): the
+ * chunk plan is cut for the workers of all parts, and tc_plan_run_part runs
+ * the chunks c with c mod nparts == part (part -1: every chunk, i.e.
+ * tc_plan_run).  Every tier is split, so the parts stay balanced whatever
+ * the cost model's error between tiers; the part counts sum to the total. */
+int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
+                         const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n,
+                         int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, int32_t nparts,
+                         tc_plan_t* plan, tc_stream_t stream);
+int tc_plan_run_part(tc_plan_t plan, int32_t part, unsigned long long* out, tc_stream_t stream);
+
 /* Generic engine over k "virtual owners": owner x probes the table list
  * N^_{owner_map[x]} (owner_map NULL: identity) with segments
  * segs[row_indptr[x] .. row_indptr[x+1]) (int32 pairs into `pool`); cost_prefix

@@ -34,6 +34,9 @@ _SIGS = {
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_plan_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_vp), _vp],
     "tc_plan_run": [_vp, _vp, _vp],
+    "tc_plan_middle_parts": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _i32, ctypes.POINTER(_vp),
+                             _vp],
+    "tc_plan_run_part": [_vp, _i32, _vp, _vp],
     "tc_plan_free": [_vp],
     "tc_count_owners": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp],
     "tc_tile_pull": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],

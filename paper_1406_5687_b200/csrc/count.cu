@@ -468,6 +468,11 @@ struct EngineArgs {
   // tab_indptr -> first / last table id).
   const int4* desc_a;       // (u, d, first id, id span)
   const longlong2* desc_b;  // (table offset t0, physical - tier-local segment index)
+  // Chunk interleave: queue ticket q claims chunk q * stride + part, so
+  // `stride` devices holding the same plan split every tier's chunks
+  // between them (replicated multi-GPU count); 1 / 0 runs them all.
+  int stride = 1;
+  int part = 0;
 };
 
 struct OwnerRef {
@@ -571,7 +576,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
 
   for (;;) {
     int c = 0;
-    if (lane == 0) c = atomicAdd(a.queue, 1);
+    if (lane == 0) c = atomicAdd(a.queue, 1) * a.stride + a.part;
     c = __shfl_sync(FULL, c, 0);
     if (c >= nch) break;
     int64_t r = a.chunk_r[c];
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Seg
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      s_chunk = atomicAdd(a.queue, 1);
+      s_chunk = atomicAdd(a.queue, 1) * a.stride + a.part;
       s_next = 0;
     }
     __syncthreads();
@@ -1041,7 +1046,7 @@ template <class Segs, class Alloc>
 EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const int64_t* row_indptr,
                             const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* pool, int64_t x0,
                             int64_t x1, const int64_t* bucket_bounds, int nbuckets, Segs segs, cudaStream_t s,
-                            const int32_t* owner_map = nullptr, int mode = 0) {
+                            const int32_t* owner_map = nullptr, int mode = 0, int parts = 1) {
   const TierShape& ts = tier_shape();
   const int64_t nx = x1 - x0;
   const int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
@@ -1074,7 +1079,9 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
     check_launch();
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, len, vrow, nx + 1, s));
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, cst, vcost, nx + 1, s));
-    const int nmax = 10 * ts.workers[k] + 8;
+    // planned for the workers of all `parts` devices that split the chunks
+    const int nW = ts.workers[k] * parts;
+    const int nmax = 10 * nW + 8;
     int64_t* chunk_r = al.template alloc<int64_t>(nmax + 1);
     int32_t* chunk_x = al.template alloc<int32_t>(nmax);
     int* ctl = al.template alloc<int>(2);  // [0] nchunks, [1] queue
@@ -1093,11 +1100,9 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
       TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp3, scost, sp, nseg + 1, s));
       void* t3 = tmp_sc.bytes(tmp3);
       TC_CUDA(cub::DeviceScan::ExclusiveSum(t3, tmp3, scost, sp, nseg + 1, s));
-      k_plan_seg<<<grid_for(nmax + 1, 256), 256, 0, s>>>(sp, nseg, vrow, nx, ts.workers[k], nmax, chunk_r, chunk_x,
-                                                         ctl);
+      k_plan_seg<<<grid_for(nmax + 1, 256), 256, 0, s>>>(sp, nseg, vrow, nx, nW, nmax, chunk_r, chunk_x, ctl);
     } else {
-      k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(vcost, vrow, 0, nx, ts.workers[k], nmax, chunk_r, chunk_x, ctl,
-                                                     mode);
+      k_plan<<<grid_for(nmax + 1, 256), 256, 0, s>>>(vcost, vrow, 0, nx, nW, nmax, chunk_r, chunk_x, ctl, mode);
     }
     check_launch();
     const int64_t lo = k == 0 ? 0 : (k == 1 ? c0 : c1);
@@ -1118,10 +1123,13 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
 // Launches the non-empty tiers (queue counters reset first); `out` must be
 // zeroed by the caller.
 template <class Segs>
-void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStream_t s) {
+void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStream_t s, int part = 0,
+                   int stride = 1) {
   const TierShape& ts = tier_shape();
   for (int k = 0; k < 3; ++k) {
     L.args[k].out = out;
+    L.args[k].part = part;
+    L.args[k].stride = stride;
     if (L.hsz[k]) TC_CUDA(cudaMemsetAsync(L.queue[k], 0, sizeof(int), s));
   }
   if (g_time_engine) {
@@ -1186,6 +1194,7 @@ struct MiddlePlan {
   int caps[3];
   Persist mem;
   EngineLaunch L;
+  int parts = 1;  // devices the chunk plan is cut for (tc_plan_middle_parts)
 };
 
 static void plan_build(MiddlePlan& P, cudaStream_t s) {
@@ -1199,7 +1208,7 @@ static void plan_build(MiddlePlan& P, cudaStream_t s) {
   Scratch sc(s);
   P.L = prepare_engine(P.mem, sc, P.rev_cost, P.rev_indptr, P.tab_indptr, P.tab_indices, P.pool, P.u0, P.u1,
                        P.bucket_bounds, P.nbuckets, PullSegs{reinterpret_cast<const int2*>(P.rev_seg)}, s,
-                       nullptr, 1);
+                       nullptr, 1, P.parts);
   sync_stream(s);
 }
 
@@ -1313,19 +1322,20 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
   });
 }
 
-int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
+int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
                    const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
-                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
-                   tc_stream_t stream) {
+                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, int32_t nparts,
+                         tc_plan_t* plan, tc_stream_t stream) {
   return tcb::guarded([&] {
     TC_REQUIRE(plan != nullptr, TC_EINVAL, "plan out-pointer is NULL");
     *plan = nullptr;
     TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
     TC_REQUIRE(nbuckets >= 1, TC_EINVAL, "nbuckets must be >= 1");
+    TC_REQUIRE(nparts >= 1 && nparts <= 1024, TC_EINVAL, "nparts must be in [1, 1024]");
     TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
     TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned");
     auto* P = new tcb::MiddlePlan{tab_indptr, rev_indptr, rev_cost, bucket_bounds, tab_indices, rev_seg, pool,
-                                  n, u0, u1, nbuckets, {0, 0, 0}, {}, {}};
+                                  n, u0, u1, nbuckets, {0, 0, 0}, {}, {}, nparts};
     try {
       tcb::plan_build(*P, (cudaStream_t)stream);
     } catch (...) {
@@ -1336,17 +1346,32 @@ int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const 
   });
 }
 
-int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream) {
+int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
+                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
+                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
+                   tc_stream_t stream) {
+  return tc_plan_middle_parts(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, n, u0, u1,
+                              bucket_bounds, nbuckets, 1, plan, stream);
+}
+
+int tc_plan_run_part(tc_plan_t plan, int32_t part, unsigned long long* out, tc_stream_t stream) {
   return tcb::guarded([&] {
     TC_REQUIRE(plan != nullptr, TC_EINVAL, "NULL plan");
     auto* P = reinterpret_cast<tcb::MiddlePlan*>(plan);
+    TC_REQUIRE(part >= -1 && part < P->parts, TC_EINVAL, "part out of range");
     cudaStream_t s = (cudaStream_t)stream;
     if (P->caps[0] != tcb::g_warp_cap || P->caps[1] != tcb::g_mid_cap || P->caps[2] != tcb::g_big_cap)
       tcb::plan_build(*P, s);
     TC_CUDA(cudaMemsetAsync(out, 0, P->nbuckets * sizeof(unsigned long long), s));
     if (P->u1 <= P->u0) return;
-    tcb::launch_engine(P->L, out, tcb::PullSegs{reinterpret_cast<const int2*>(P->rev_seg)}, s);
+    const tcb::PullSegs segs{reinterpret_cast<const int2*>(P->rev_seg)};
+    if (part < 0) tcb::launch_engine(P->L, out, segs, s);  // every chunk
+    else tcb::launch_engine(P->L, out, segs, s, part, P->parts);
   });
+}
+
+int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream) {
+  return tc_plan_run_part(plan, -1, out, stream);
 }
 
 int tc_plan_free(tc_plan_t plan) {

@@ -44,17 +44,17 @@ class _MiddlePlan:
 
     __slots__ = ("handle",)
 
-    def __init__(self, g: Graph, u0: int, u1: int):
+    def __init__(self, g: Graph, u0: int, u1: int, parts: int = 1):
         import ctypes
 
         h = ctypes.c_void_p()
-        _lib.call("tc_plan_middle", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(g._rev_indptr),
+        _lib.call("tc_plan_middle_parts", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(g._rev_indptr),
                   _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost), _lib.ptr(g.eff_indices), g.n, u0, u1, None, 1,
-                  ctypes.byref(h), _lib.stream())
+                  int(parts), ctypes.byref(h), _lib.stream())
         self.handle = h
 
-    def run(self, out):
-        _lib.call("tc_plan_run", self.handle, _lib.ptr(out), _lib.stream())
+    def run(self, out, part=-1):
+        _lib.call("tc_plan_run_part", self.handle, int(part), _lib.ptr(out), _lib.stream())
 
     def __del__(self):
         try:
@@ -95,6 +95,25 @@ def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
               _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost),
               _lib.ptr(g.eff_indices), g.n, int(u0), int(u1), _lib.ptr(bounds), k, _lib.ptr(out),
               _lib.stream())
+    return out
+
+
+def count_middle_part(g: Graph, part: int, parts: int, out=None):
+    """The chunks c with c mod parts == part of the whole-graph middle-vertex
+    engine plan, cut for `parts` devices (tc_plan_middle_parts): the
+    replicated multi-GPU count, where every rank holds the graph and the
+    rank partials sum (NCCL all-reduce) to the total.  Every tier is split
+    between the parts, so they stay balanced whatever the cost model's
+    error between tiers (dynamic_lb.py:68-109 across ranks)."""
+    if not 0 <= part < parts:
+        raise ValueError("part must be in [0, parts)")
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64, device=g.eff_indptr.device)
+    key = ("middle_plan_parts", int(parts))
+    plan = g._cache.get(key)
+    if plan is None:
+        plan = g._cache[key] = _MiddlePlan(g, 0, g.n, parts)
+    plan.run(out, part)
     return out
 
 

@@ -14,7 +14,7 @@ import torch.distributed as dist
 import paper_1406_5687_b200 as tcb
 from paper_1406_5687_b200.distributed import count_space_direct_dist, count_space_surrogate_dist
 from paper_1406_5687_b200.graph_io import rmat_edges
-from paper_1406_5687_b200.sequential import count_middle
+from paper_1406_5687_b200.sequential import count_middle, count_middle_part
 
 pytestmark = pytest.mark.gpu
 
@@ -43,6 +43,9 @@ def test_nccl_world1_schemes(nccl_group):
     assert total == T and met.triangles == T
     total, met = count_space_direct_dist(g)
     assert total == T and met.triangles == T
-    c = count_middle(g, 0, g.n)  # bench.py's replicated step: range count + all_reduce
+    c = count_middle(g, 0, g.n)  # range count + all_reduce
+    dist.all_reduce(c)
+    assert int(c.item()) == T
+    c = count_middle_part(g, 0, 1)  # bench.py's replicated step at world size 1
     dist.all_reduce(c)
     assert int(c.item()) == T

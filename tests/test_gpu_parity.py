@@ -11,7 +11,7 @@ from conftest import SMALL, SMALL_NAMES
 import paper_1406_5687_b200 as tcb
 from paper_1406_5687_b200 import graph as G
 from paper_1406_5687_b200.graph_io import er_edges, pa_edges_host, rmat_edges
-from paper_1406_5687_b200.sequential import count_lowest, count_middle
+from paper_1406_5687_b200.sequential import count_lowest, count_middle, count_middle_part
 from oracle import gen_twin
 from oracle import oracle as O
 
@@ -336,6 +336,8 @@ def test_engine_tiers_forced(caps):
             assert [m.triangles for m in rr.metrics] == case["surr_tri_3"].tolist(), name
             b = torch.as_tensor(case["bounds_predsum_5"]).cuda()
             assert host(count_lowest(g, 0, g.n, bounds=b)).tolist() == case["lowest_5"].tolist(), name
+            for parts in (2, 3):
+                assert sum(int(count_middle_part(g, p, parts).item()) for p in range(parts)) == T, (name, parts)
     finally:
         L.tc_set_tuning(0, 256)
         L.tc_set_tuning(2, 512)
@@ -635,3 +637,26 @@ def test_partitioned_schemes_tiny_graphs(known, name):
         else:
             tot, rr = tcb.count_dynamic(g, P)
             assert (tot, len(rr.metrics)) == (want["total"], want["nmetrics"])
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 8, 13])
+def test_replicated_parts_sum_to_total(parts):
+    """bench.py's replicated multi-GPU count: the rank shares of the
+    interleaved plan (tc_plan_middle_parts / tc_plan_run_part) are disjoint
+    and cover every chunk, so they sum to the reference's total on every
+    fixture, on an R-MAT graph with hub (block tier) owners, and on graphs
+    smaller than the number of parts."""
+    for name in SMALL_NAMES:
+        _, g = graph_of(name)
+        T = int(SMALL[name]["T"][0])
+        got = [int(count_middle_part(g, p, parts).item()) for p in range(parts)]
+        assert sum(got) == T and min(got) >= 0, (name, got)
+    raw = rmat_edges(16, 16, 3)
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=1 << 16, edges=raw)))
+    T = tcb.count_triangles_seq(g)
+    got = [int(count_middle_part(g, p, parts).item()) for p in range(parts)]
+    assert sum(got) == T
+    if parts > 1:  # every part gets work on a graph this size
+        assert min(got) > 0, got
+    with pytest.raises(ValueError):
+        count_middle_part(g, parts, parts)
