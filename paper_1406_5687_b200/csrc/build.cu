@@ -170,6 +170,15 @@ __global__ void k_pack_pairs(const int32_t* __restrict__ e, int64_t m,
   if ((threadIdx.x & 31) == 0 && f) atomicOr(order_flags, f);
 }
 
+// Publishes a chunk's order flags and the running largest label to mapped
+// pinned host memory (two words over PCIe; no copy-engine round trip).
+__global__ void k_publish_flags(const unsigned* __restrict__ flags, const int* __restrict__ mx,
+                                volatile unsigned* host) {
+  host[0] = *flags;
+  host[1] = (unsigned)*mx;
+  __threadfence_system();
+}
+
 // (lo << b | hi) key -> (lo, hi) pair, written by the unique pass itself.
 struct UnpackKey {
   int b;
@@ -724,6 +733,40 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
                                         KeyLess(), s));
     stack.push_back(Run{r1.o, r1.len + r2.len, z, std::max(r1.level, r2.level) + 1});
   };
+  // Chunk c's flags (sortedness, largest label so far) travel to pinned host
+  // memory behind its pack kernel and the host waits on one event for both
+  // (one short round trip per chunk; the copy stream runs on meanwhile).  The
+  // sort must follow chunk c's passes before the stream waits for chunk c+1's
+  // copy, or it would queue behind that copy.
+  static unsigned* hflags[64] = {};
+  static unsigned* dflags[64] = {};  // device view of the mapped hflags
+  static cudaEvent_t fev[64][kMaxChunks] = {};
+  if (!hflags[d]) {
+    TC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hflags[d]), 2 * kMaxChunks * sizeof(unsigned),
+                          cudaHostAllocMapped));
+    TC_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflags[d]), hflags[d], 0));
+    for (auto& e : fev[d]) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  auto sort_chunk = [&](int c) {
+    const int64_t o = c * per, mc = std::min(per, m_raw - o);
+    TC_CUDA(cudaEventSynchronize(fev[d][c]));
+    const unsigned f = hflags[d][2 * c], hmax = hflags[d][2 * c + 1];
+    if ((int)hmax < 0) {  // a negative label: no runs (the device path reports it)
+      runs = false;
+      return;
+    }
+    any_loop |= (f & 4u) != 0;  // a self-loop packs as ~0: sorts last, one survives unique
+    const int hi_bits = 32 + std::max(1, bits_for((uint64_t)hmax));
+    size_t tb = sort_tmp;
+    if (!(f & 1u))  // already sorted
+      TC_CUDA(cudaMemcpyAsync(kb + o, ka + o, mc * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    else if (!(f & 2u))  // larger endpoints non-decreasing: a stable sort by the smaller one suffices
+      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 32, hi_bits, s));
+    else  // (e.g. a generator's seed clique) the whole key
+      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 0, hi_bits, s));
+    stack.push_back(Run{o, mc, kb, 0});
+    while (stack.size() >= 2 && stack[stack.size() - 1].level == stack[stack.size() - 2].level) merge_top();
+  };
   for (int c = 0; c < nch; ++c) {
     const int64_t o = c * per, mc = std::min(per, m_raw - o);
     if (mc <= 0) break;
@@ -732,29 +775,15 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
     check_launch();
     k_first_pos<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, fp, o, cap, mm + 2, deg);
     check_launch();
-    if (!runs) continue;
-    k_pack_pairs<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, nullptr, 32, ka + o,
-                                                                     cflags + c);
-    check_launch();
-    unsigned hf[2] = {0, 0};  // (chunk flags, largest label so far); the copy stream runs on meanwhile
-    TC_CUDA(cudaMemcpyAsync(&hf[0], cflags + c, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaMemcpyAsync(&hf[1], mm + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    sync_stream(s);
-    if ((int)hf[1] < 0) {
-      runs = false;
-      continue;
+    if (runs) {
+      k_pack_pairs<<<grid_for(mc, kBlock, sms * 16), kBlock, 0, s>>>(dev + 2 * o, mc, nullptr, 32, ka + o,
+                                                                       cflags + c);
+      check_launch();
+      k_publish_flags<<<1, 1, 0, s>>>(cflags + c, mm + 1, dflags[d] + 2 * c);
+      check_launch();
+      TC_CUDA(cudaEventRecord(fev[d][c], s));
+      sort_chunk(c);
     }
-    any_loop |= (hf[0] & 4u) != 0;  // a self-loop packs as ~0: sorts last, one survives unique
-    const int hi_bits = 32 + std::max(1, bits_for((uint64_t)hf[1]));
-    size_t tb = sort_tmp;
-    if (!(hf[0] & 1u))  // already sorted
-      TC_CUDA(cudaMemcpyAsync(kb + o, ka + o, mc * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-    else if (!(hf[0] & 2u))  // larger endpoints non-decreasing: a stable sort by the smaller one suffices
-      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 32, hi_bits, s));
-    else  // (e.g. a generator's seed clique) the whole key
-      TC_CUDA(cub::DeviceRadixSort::SortKeys(sort_ws, tb, ka + o, kb + o, mc, 0, hi_bits, s));
-    stack.push_back(Run{o, mc, kb, 0});
-    while (stack.size() >= 2 && stack[stack.size() - 1].level == stack[stack.size() - 2].level) merge_top();
   }
   int hmm[3];
   TC_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
