@@ -219,17 +219,36 @@ __global__ void k_copy_i32(const int32_t* __restrict__ a, int32_t* b, int64_t n)
 
 
 // Orientation (graph.py:113-125), counting-sort form.  Pass 1: every pair
-// becomes (lo, hi) in canonical labels (kept for pass 2) and adds 1 to row
-// lo's size (fire-and-forget atomics).
+// becomes (lo, hi) in canonical labels (kept for pass 2) and counts one
+// predecessor of hi.  Row lo's size is then deg - predecessors (k_eff_counts):
+// every pair gives one endpoint slot to its lo row and one to hi, so this
+// holds with duplicates and self-loops too.  Counting hi rather than lo lets
+// the atomics aggregate over runs: a normalized list is sorted by its
+// smaller original label, which is usually the higher-degree endpoint, so
+// consecutive pairs share hi (cfg 2: 50 M L2 atomics became a few M).
 __global__ void k_orient_count(const int32_t* __restrict__ e, int64_t m, const int32_t* __restrict__ relabel,
-                               int2* __restrict__ lohi, unsigned long long* cnt) {
-  GRID_STRIDE(i, m) {
-    const int2 p = reinterpret_cast<const int2*>(e)[i];
-    const int32_t x = relabel[p.x], y = relabel[p.y];
-    const int2 k = make_int2(min(x, y), max(x, y));
-    lohi[i] = k;
-    atomicAdd(&cnt[k.x], 1ull);
+                               int2* __restrict__ lohi, int32_t* hicnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < m;
+    int2 k = make_int2(0, 0);
+    if (valid) {
+      const int2 p = reinterpret_cast<const int2*>(e)[i];
+      const int32_t x = relabel[p.x], y = relabel[p.y];
+      k = make_int2(min(x, y), max(x, y));
+      lohi[i] = k;
+    }
+    int st = 0, c;
+    if ((c = warp_run_end(k.y, valid, lane, &st))) atomicAdd(&hicnt[k.y], c);
   }
+}
+
+// Forward row sizes (int64, for the offsets scan): deg - predecessors.
+__global__ void k_eff_counts(const int32_t* __restrict__ deg_orig, const int32_t* __restrict__ orig_ids,
+                             const int32_t* __restrict__ hicnt, int64_t n, long long* cnt) {
+  GRID_STRIDE(v, n + 1) cnt[v] = v < n ? (long long)(deg_orig[orig_ids[v]] - hicnt[v]) : 0;
 }
 
 // Pass 2: hi goes to a slot of row lo claimed with an atomic cursor.  The
@@ -863,15 +882,18 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   // phased counting scatter, then every row sorted (segmented sort)
   int64_t* bounds = sc.alloc<int64_t>(8);
   {
-    unsigned long long* cnt = sc.alloc<unsigned long long>(n + 1);
-    TC_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(unsigned long long), s));
+    long long* cnt = sc.alloc<long long>(n + 1);
+    int32_t* hicnt = sc.alloc<int32_t>(n);
+    TC_CUDA(cudaMemsetAsync(hicnt, 0, n * sizeof(int32_t), s));
     int2* lohi = sc.alloc<int2>(m);
     if (m) {
-      k_orient_count<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, lohi, cnt);
+      k_orient_count<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(edges, m, relabel, lohi, hicnt);
       check_launch();
     }
+    k_eff_counts<<<grid_for(n + 1, kBlock), kBlock, 0, s>>>(deg_orig, orig_ids, hicnt, n, cnt);
+    check_launch();
     size_t tmp = 0;
-    auto* cin = reinterpret_cast<long long*>(cnt);
+    auto* cin = cnt;
     auto* cout = reinterpret_cast<long long*>(eff_indptr);
     TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cin, cout, n + 1, s));
     void* t = sc.bytes(tmp);
