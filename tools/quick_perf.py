@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="cfg2")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--lowest", action="store_true")
+ap.add_argument("--no-tiled", action="store_true")
 a = ap.parse_args()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for cfg in a.configs.split(","):
@@ -32,14 +33,16 @@ for cfg in a.configs.split(","):
         e.record()
         torch.cuda.synchronize()
     build_ms = s.elapsed_time(e)
-    engines = [("middle", lambda: count_middle(g, tiled=False)), ("tiled", lambda: count_middle(g, tiled=True))]
+    engines = [("middle", lambda: count_middle(g, tiled=False))]
+    engines += [] if a.no_tiled else [("tiled", lambda: count_middle(g, tiled=True))]
     engines += [("lowest", lambda: count_lowest(g))] if a.lowest else []
     from paper_1406_5687_b200.graph import tiled_index
     import paper_1406_5687_b200.graph as G
     if G.TILE_IDS == 0:
         G.TILE_IDS = 8 << 20
-    ti = tiled_index(g, 0, g.n)
-    print(f"{cfg}: tiles={ti.ntiles} virtual owners={ti.k}", flush=True)
+    if not a.no_tiled:
+        ti = tiled_index(g, 0, g.n)
+        print(f"{cfg}: tiles={ti.ntiles} virtual owners={ti.k}", flush=True)
     for name, fn in engines:
         T = int(fn().item())
         _lib.lib().tc_engine_timing(1, None, None, None)
