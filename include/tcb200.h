@@ -129,7 +129,10 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
  * once (synchronises); tc_plan_run then only zeroes `out` and launches the
  * engine (no host synchronisation, graph-capturable).  The plan keeps the
  * argument pointers -- the caller keeps those arrays alive and unchanged --
- * and re-plans itself if tc_set_tuning changed the tier caps. */
+ * and re-plans itself if tc_set_tuning changed the tier caps.  Planning does
+ * not synchronise at its end: runs wait on the plan's event (a run captured
+ * into a CUDA graph must be captured after the planning stream has
+ * synchronised). */
 typedef struct tc_plan_s* tc_plan_t;
 int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
                    const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,

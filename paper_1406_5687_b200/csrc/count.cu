@@ -1195,6 +1195,10 @@ struct MiddlePlan {
   Persist mem;
   EngineLaunch L;
   int parts = 1;  // devices the chunk plan is cut for (tc_plan_middle_parts)
+  cudaEvent_t ready = nullptr;  // recorded after the planning kernels; runs on any stream wait on it
+  ~MiddlePlan() {
+    if (ready) cudaEventDestroy(ready);
+  }
 };
 
 static void plan_build(MiddlePlan& P, cudaStream_t s) {
@@ -1209,7 +1213,10 @@ static void plan_build(MiddlePlan& P, cudaStream_t s) {
   P.L = prepare_engine(P.mem, sc, P.rev_cost, P.rev_indptr, P.tab_indptr, P.tab_indices, P.pool, P.u0, P.u1,
                        P.bucket_bounds, P.nbuckets, PullSegs{reinterpret_cast<const int2*>(P.rev_seg)}, s,
                        nullptr, 1, P.parts);
-  sync_stream(s);
+  // no host synchronisation: a run waits on this event (pool memory of the
+  // plan becomes valid on the run's stream through it)
+  if (!P.ready) TC_CUDA(cudaEventCreateWithFlags(&P.ready, cudaEventDisableTiming));
+  TC_CUDA(cudaEventRecord(P.ready, s));
 }
 
 void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
@@ -1364,6 +1371,9 @@ int tc_plan_run_part(tc_plan_t plan, int32_t part, unsigned long long* out, tc_s
       tcb::plan_build(*P, s);
     TC_CUDA(cudaMemsetAsync(out, 0, P->nbuckets * sizeof(unsigned long long), s));
     if (P->u1 <= P->u0) return;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    TC_CUDA(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) TC_CUDA(cudaStreamWaitEvent(s, P->ready, 0));
     const tcb::PullSegs segs{reinterpret_cast<const int2*>(P->rev_seg)};
     if (part < 0) tcb::launch_engine(P->L, out, segs, s);  // every chunk
     else tcb::launch_engine(P->L, out, segs, s, part, P->parts);
