@@ -68,10 +68,22 @@ static constexpr int kLbMid = 8;          // mid tier buckets: 2^8 x 4 ids (4 KB
 static constexpr int kMidWarps = 4;       // mid tier: warps per block (8 KB private slices)
 static constexpr int kBigThreads = 512;   // block tier
 static constexpr int kBigWarps = kBigThreads / 32;
-static constexpr int kBigCap = 4096;      // block tier: ids per staged table
+#ifndef TCB_BIG_CAP
+#define TCB_BIG_CAP 4096
+#endif
+#ifndef TCB_BIG_LB
+#define TCB_BIG_LB 11
+#endif
+#ifndef TCB_POS_CAP
+#define TCB_POS_CAP 512
+#endif
+#ifndef TCB_BIG_MINB
+#define TCB_BIG_MINB 2
+#endif
+static constexpr int kBigCap = TCB_BIG_CAP;  // block tier: ids per staged table
 static constexpr int kLwBig = 13;         // block tier filter: 2^13 words = 256K bits (32 KB)
-static constexpr int kLbBig = 11;         // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
-static constexpr int kPosCap = 512;       // block tier: per-warp queue of filter hits
+static constexpr int kLbBig = TCB_BIG_LB;  // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
+static constexpr int kPosCap = TCB_POS_CAP;  // block tier: per-warp queue of filter hits
 static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
 static constexpr int kSbWords = 32;  // per-warp bitmap of segment starts: groups of <= 1024 chunks
 static constexpr int kSegTab = 32 + kSbWords / 4;  // int4 per warp: 32 segment entries + the start bitmap
@@ -641,7 +653,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
 // Block tier: owners with d > d_lo (the mid tier's cap).  The block stages the owner's table
 // once per chunk-owner and its 16 warps stream groups of 32 segments.
 template <class Segs>
-__global__ void __launch_bounds__(kBigThreads, 2) k_engine_big(EngineArgs a, Segs segs) {
+__global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(EngineArgs a, Segs segs) {
   extern __shared__ __align__(16) unsigned char big_smem[];
   uint32_t* bm = reinterpret_cast<uint32_t*>(big_smem);
   int4* bkt = reinterpret_cast<int4*>(big_smem + (sizeof(uint32_t) << kLwBig));
