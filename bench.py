@@ -282,17 +282,21 @@ def _gpu_arm_core(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1 and not dist.is_initialized():
+    # TCB_BENCH_DIST=1 runs the N-GPU code path (process group, NCCL
+    # collectives, rank shares) at world size 1: a check of the multi-GPU
+    # step on a one-GPU box
+    distp = world > 1 or os.environ.get("TCB_BENCH_DIST") == "1"
+    if distp and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     def barrier():
-        if world > 1:
+        if distp:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not distp:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -310,7 +314,7 @@ def _gpu_arm_core(args):
     n, m = g.n, g.m
     W = int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum())
 
-    mode = args.mode if world > 1 else "single"
+    mode = args.mode if distp else "single"
     out = torch.empty(1, dtype=torch.int64, device=dev)
     if mode in ("surrogate", "direct"):
         from paper_1406_5687_b200.distributed import direct_rank, shard_of, surrogate_rank
@@ -328,7 +332,7 @@ def _gpu_arm_core(args):
             total, _ = rank_fn(shard, sb)
             out.fill_(total)
             return out
-        if world > 1:  # replicated: this rank's interleaved share of the engine's chunks
+        if distp:  # replicated: this rank's interleaved share of the engine's chunks
             count_middle_part(g, rank, world, out=out)
             dist.all_reduce(out)
         else:
@@ -386,7 +390,7 @@ def _gpu_arm_core(args):
             gg = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw_host)))
             if mode in ("surrogate", "direct"):
                 tri, _ = rank_fn(shard_of(gg, int(sb[rank]), int(sb[rank + 1])), sb)
-            elif world > 1:
+            elif distp:
                 c = count_middle_part(gg, rank, world)
                 dist.all_reduce(c)
                 tri = int(c.item())
@@ -408,7 +412,7 @@ def _gpu_arm_core(args):
             cpu = cpu_baseline_leg(raw_host, args.cpu_target_s)
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": UNIT, "error": repr(exc)}
-    if world > 1:
+    if distp:
         dist.destroy_process_group()
     if rank != 0:
         return None

@@ -49,3 +49,26 @@ def test_nccl_world1_schemes(nccl_group):
     c = count_middle_part(g, 0, 1)  # bench.py's replicated step at world size 1
     dist.all_reduce(c)
     assert int(c.item()) == T
+
+
+@pytest.mark.parametrize("mode", ["replicated", "surrogate", "direct"])
+def test_bench_multi_gpu_path_world1(mode, tmp_path):
+    """bench.py's N-GPU step (torchrun, NCCL process group, the rank's share
+    of the count, all-reduce, max over ranks) at world size 1
+    (TCB_BENCH_DIST=1): the JSON line carries the reference's total."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TCB_BENCH_DIST="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(repo, "bench.py"),
+           "--gpus", "1", "--steps", "2", "--warmup", "3", "--mode", mode, "--no-e2e", "--no-cpu-baseline",
+           "--config", "cfg1"]
+    out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["config"]["triangles"] == 722 and line["n_gpus"] == 1
+    assert {"replicated": "replicated", "surrogate": "surrogate", "direct": "pull"}[mode] in line["config"]["parallelism"]

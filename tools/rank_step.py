@@ -105,6 +105,12 @@ print(f"{a.config}: 1 GPU count {t1:.3f} ms (wall, incl. host overhead)", flush=
 for P in [int(x) for x in a.ranks.split(",")]:
     sb = range_bounds(partition_ranges(g, tcb.CostKind.PRED_SUM, P))
     surr = surrogate_step(P, sb) if "surrogate" in MODES else [0.0]
+    if "surrogate" in MODES:  # the same scheme on ranges balanced by the engine's own cost prefix
+        ucost = (g._rev_cost[1:] - g._rev_cost[:-1]).contiguous()
+        eb = balanced_bounds(ucost, 0, g.n, P).cpu().numpy()
+        se = surrogate_step(P, eb)
+        print(f"P={P}: surrogate[engine-cost ranges] max {max(se):.3f} ms (ranks {' '.join(f'{x:.2f}' for x in se)}) "
+              f"-> eff {t1 / (P * max(se)):.2f}; [predsum ranges] ranks {' '.join(f'{x:.2f}' for x in surr)}", flush=True)
     if "direct" in MODES:
         direct_step(P)
     rep = [0.0]
@@ -113,6 +119,8 @@ for P in [int(x) for x in a.ranks.split(",")]:
         ub = balanced_bounds(ucost, 0, g.n, P).cpu().numpy()
         rep = [timed(lambda r=r: count_middle(g, int(ub[r]), int(ub[r + 1]), out=out)) for r in range(P)]
     # replicated, interleaved: rank r runs chunks c = r (mod P) of the plan cut for P GPUs
+    if "replicated" not in MODES:
+        continue
     tot = 0
     ilv = []
     for r in range(P):
