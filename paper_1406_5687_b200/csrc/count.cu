@@ -109,7 +109,7 @@ struct WarpSliceT {
 // enforced at build; owner_segments checks its pool).
 struct PullSegs {  // rev_seg int32 pairs (start, end) into the pool
   const int2* seg;
-  __device__ __forceinline__ void get(int64_t r, int& s, int& e) const {
+  __device__ __forceinline__ void get(int r, int& s, int& e) const {
     const int2 x = __ldg(&seg[r]);
     s = x.x;
     e = x.y;
@@ -119,7 +119,7 @@ struct PullSegs {  // rev_seg int32 pairs (start, end) into the pool
 struct PushSegs {  // forward edge e of v -> N^_u, u = indices[e]
   const int64_t* indptr;
   const int32_t* indices;
-  __device__ __forceinline__ void get(int64_t r, int& s, int& e) const {
+  __device__ __forceinline__ void get(int r, int& s, int& e) const {
     int32_t u = __ldg(&indices[r]);
     s = (int)__ldg(&indptr[u]);
     e = (int)__ldg(&indptr[u + 1]);
@@ -399,8 +399,8 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 // mostly longer than 1024 chunks and keep the ballot/redux resolution).
 template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
-                                             int64_t g0, int64_t g1, int lane, int& npos, uint32_t& cnt,
-                                             int4* segtab, int64_t pf_end = 0) {
+                                             int g0, int g1, int lane, int& npos, uint32_t& cnt,
+                                             int4* segtab, int pf_end = 0) {
   const unsigned FULL = 0xffffffffu;
   int s = 0, e = 0;
   if (g0 + lane < g1) segs.get(g0 + lane, s, e);
@@ -545,6 +545,18 @@ __device__ __forceinline__ int64_t advance_owner(const EngineArgs& a, int64_t x,
   }
 }
 
+// advance_owner in 32-bit indices (tier-local owners and segment rows are
+// < 2^31): the warp tiers' loop state then fits fewer registers.
+__device__ __forceinline__ int advance_owner32(const EngineArgs& a, int x, int r, int lane) {
+  for (;;) {
+    const int idx = x + 1 + lane;
+    const int nx = (idx <= a.n_owner) ? (int)__ldg(&a.row_indptr[idx]) : INT_MAX;
+    const unsigned past = __ballot_sync(0xffffffffu, nx > r);
+    if (past) return x + __ffs(past) - 1;
+    x += 32;
+  }
+}
+
 // Per-warp accumulation, flushed per bucket.
 struct Acc {
   unsigned long long acc = 0;  // same on all lanes
@@ -591,17 +603,18 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
     if (lane == 0) c = atomicAdd(a.queue, 1) * a.stride + a.part;
     c = __shfl_sync(FULL, c, 0);
     if (c >= nch) break;
-    int64_t r = a.chunk_r[c];
-    const int64_t r1 = a.chunk_r[c + 1];
-    int64_t x = a.chunk_x[c];
+    int r = (int)a.chunk_r[c];  // 32-bit loop state (segment rows and owners < 2^31)
+    const int r1 = (int)a.chunk_r[c + 1];
+    int x = a.chunk_x[c];
     while (r < r1) {
-      x = advance_owner(a, x, r, lane);
-      const int64_t xe_row = __ldg(&a.row_indptr[x + 1]);
-      const int64_t rb = min(xe_row, r1);
-      const int64_t ra = r;
+      x = advance_owner32(a, x, r, lane);
+      const int xe_row = (int)__ldg(&a.row_indptr[x + 1]);
+      const int rb = min(xe_row, r1);
+      const int ra = r;
       r = rb;
       const OwnerRef ow = resolve_owner(a, x);
-      const int64_t u = ow.u;
+      const int u = (int)ow.u;
+      const int so = (int)ow.seg_off;
       const int d = ow.d;  // in (d_lo, d_hi]: the list holds this tier's owners only
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + ow.t0;
@@ -617,9 +630,9 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         __syncwarp();
         Table t{sl.bm, nullptr, nullptr, nullptr, d, 0, tlo, 0, 0, span};
         int npos = 0;
-        for (int64_t g = ra; g < rb; g += 32)
-          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                       lane, npos, acc.cnt, segtab, rb + ow.seg_off);
+        for (int g = ra; g < rb; g += 32)
+          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+                                                                    lane, npos, acc.cnt, segtab, rb + so);
         __syncwarp();
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
         __syncwarp();
@@ -638,9 +651,9 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       Table t{sl.bm, nullptr, sl.bkt, nullptr, d, lb, 0, 0, disp, 0};
       __syncwarp();
       int npos = 0;
-      for (int64_t g = ra; g < rb; g += 32)
-        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off,
-                                                      lane, npos, acc.cnt, segtab, rb + ow.seg_off);
+      for (int g = ra; g < rb; g += 32)
+        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+                                                                   lane, npos, acc.cnt, segtab, rb + so);
       __syncwarp();
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
       __syncwarp();
@@ -685,17 +698,18 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
     __syncthreads();
     const int c = s_chunk;
     if (c >= nch) break;
-    int64_t r = a.chunk_r[c];
-    const int64_t r1 = a.chunk_r[c + 1];
-    int64_t x = a.chunk_x[c];
+    int r = (int)a.chunk_r[c];  // 32-bit loop state, as in k_engine
+    const int r1 = (int)a.chunk_r[c + 1];
+    int x = a.chunk_x[c];
     while (r < r1) {
-      x = advance_owner(a, x, r, lane);  // same result in every warp
-      const int64_t xe_row = __ldg(&a.row_indptr[x + 1]);
-      const int64_t rb = min(xe_row, r1);
-      const int64_t ra = r;
+      x = advance_owner32(a, x, r, lane);  // same result in every warp
+      const int xe_row = (int)__ldg(&a.row_indptr[x + 1]);
+      const int rb = min(xe_row, r1);
+      const int ra = r;
       r = rb;
       const OwnerRef ow = resolve_owner(a, x);
       const int64_t u = ow.u;
+      const int so = (int)ow.seg_off;
       const int64_t d = ow.d;
       acc.to_bucket(a, u, lane);
       const int32_t* gtab = a.tab_indices + ow.t0;
@@ -743,21 +757,21 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           int gi = 0;
           if (lane == 0) gi = atomicAdd(&s_next, 1);
           gi = __shfl_sync(0xffffffffu, gi, 0);
-          const int64_t g = ra + 32 * (int64_t)gi;
+          const int g = ra + 32 * gi;
           if (g >= rb) break;
           if (staged_exact)
-            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                          acc.cnt, segtab);
           else
-            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                            acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
       } else {
         Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1]), 0, 0};
         int npos = 0;
-        for (int64_t g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kGlobal, 0, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + ow.seg_off, min(g + 32, rb) + ow.seg_off, lane, npos,
+        for (int g = ra + 32 * warp; g < rb; g += 32 * nwarps)
+          stream_group<kGlobal, 0, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                    acc.cnt, segtab);
       }
     }
