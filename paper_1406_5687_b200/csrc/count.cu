@@ -53,6 +53,9 @@ namespace tcb {
 #ifndef TCB_MID_PIPE
 #define TCB_MID_PIPE 1
 #endif
+#ifndef TCB_SEGPTR
+#define TCB_SEGPTR 1
+#endif
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
@@ -329,8 +332,14 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
       }
       const int f = b + lane;
       if (f < total) {
+#if TCB_SEGPTR
+        const int4 q = segtab[sj];  // (&pool4[delta] lo, hi, excl, endx << 8 | last mask << 4 | first mask)
+        const int4* p = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
+        v[k] = __ldg(p + f);
+#else
         const int4 q = segtab[sj];  // (delta, -, excl, endx << 8 | last mask << 4 | first mask)
         v[k] = __ldg(&pool4[q.x + f]);
+#endif
         uint32_t mk = 0xFu;
         if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
         if (f == (q.w >> 8) - 1) mk &= ((uint32_t)q.w >> 4) & 0xFu;
@@ -438,7 +447,12 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   const bool fast = kSb && total <= 32 * kSbWords;
   __syncwarp();  // the previous group's reads of segtab are done
   if (lane < nseg) {
+#if TCB_SEGPTR
+    const unsigned long long p = (unsigned long long)pool + 16ll * (long long)delta;  // chunk 0 of the flat space
+    segtab[lane] = make_int4((int)(unsigned)p, (int)(unsigned)(p >> 32), excl, (incl << 8) | (lm << 4) | fm);
+#else
     segtab[lane] = make_int4(delta, 0, excl, (incl << 8) | (lm << 4) | fm);
+#endif
     if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
   }
   __syncwarp();
