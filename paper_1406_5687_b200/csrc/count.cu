@@ -56,6 +56,9 @@ namespace tcb {
 #ifndef TCB_SEGPTR
 #define TCB_SEGPTR 1
 #endif
+#ifndef TCB_FASTSPLIT
+#define TCB_FASTSPLIT 0
+#endif
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
@@ -88,7 +91,10 @@ static constexpr int kLwBig = 13;         // block tier filter: 2^13 words = 256
 static constexpr int kLbBig = TCB_BIG_LB;  // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
 static constexpr int kPosCap = TCB_POS_CAP;  // block tier: per-warp queue of filter hits
 static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
-static constexpr int kSbWords = 32;  // per-warp bitmap of segment starts: groups of <= 1024 chunks
+#ifndef TCB_SBWORDS
+#define TCB_SBWORDS 64
+#endif
+static constexpr int kSbWords = TCB_SBWORDS;  // per-warp bitmap of segment starts: groups of <= 32 kSbWords chunks
 static constexpr int kSegTab = 32 + kSbWords / 4;  // int4 per warp: 32 segment entries + the start bitmap
 
 static constexpr size_t kBigSmem = (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
@@ -307,11 +313,12 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 // count << 2).
 // Resolves and loads the kW windows starting at chunk `base` (see
 // probe_group).
-template <int kW, bool kSb>
+template <int kW, bool kMayFast>
 __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, bool lane_seg, int excl,
                                              const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
-                                             int total, int lane, bool fast, int base, int& cbase, int4 (&v)[kW],
+                                             int total, int lane, bool fast_rt, int base, int& cbase, int4 (&v)[kW],
                                              uint32_t (&vm)[kW]) {
+  const bool fast = kMayFast && fast_rt;
   const unsigned FULL = 0xffffffffu;
 #pragma unroll
   for (int k = 0; k < kW; ++k) {
@@ -333,16 +340,16 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
       const int f = b + lane;
       if (f < total) {
 #if TCB_SEGPTR
-        const int4 q = segtab[sj];  // (&pool4[delta] lo, hi, excl, endx << 8 | last mask << 4 | first mask)
+        const int4 q = segtab[sj];  // (&pool4[delta] lo, hi, excl, (endx - 1) << 8 | last mask << 4 | first mask)
         const int4* p = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
         v[k] = __ldg(p + f);
 #else
-        const int4 q = segtab[sj];  // (delta, -, excl, endx << 8 | last mask << 4 | first mask)
+        const int4 q = segtab[sj];  // (delta, -, excl, (endx - 1) << 8 | last mask << 4 | first mask)
         v[k] = __ldg(&pool4[q.x + f]);
 #endif
         uint32_t mk = 0xFu;
         if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
-        if (f == (q.w >> 8) - 1) mk &= ((uint32_t)q.w >> 4) & 0xFu;
+        if (f == (q.w >> 8)) mk &= ((uint32_t)q.w >> 4) & 0xFu;
         vm[k] = mk;
       }
     }
@@ -359,46 +366,63 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
 // 2 kW loads per warp are in flight across the probe work.  Measured: the
 // mid tier gains (cfg 5 24.2 -> 20.6 ms), the small tier loses (cfg 2 2.49 ->
 // 2.61 ms: registers), so only the mid tier pipelines.
+template <int kKind, int kLw, int kCap, int kW, bool kFast, bool kPipe>
+__device__ __forceinline__ void probe_loop(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
+                                           const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
+                                           int total, int lane, int& npos, uint32_t& cnt, bool fast = kFast) {
+  const bool lane_seg = lane < nseg;
+  int cbase = 0;  // fast path: segments starting before the window
+  int4 v[kW];
+  uint32_t vm[kW];
+  load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, 0, cbase, v, vm);
+  for (int base = 0; base < total; base += 32 * kW) {
+    if (kPipe) {
+      int4 nv[kW];
+      uint32_t nvm[kW];
+      const int nb = base + 32 * kW;
+      if (nb < total) {
+        load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, nb, cbase, nv, nvm);
+      } else {
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+          nvm[k] = 0;
+          nv[k] = make_int4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
+      if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+#pragma unroll
+      for (int k = 0; k < kW; ++k) {
+        v[k] = nv[k];
+        vm[k] = nvm[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
+      if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+      if (base + 32 * kW < total)
+        load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, base + 32 * kW, cbase, v,
+                                 vm);
+    }
+  }
+}
+
+// The segment resolution path (start bitmap or ballot) is chosen once per
+// group, so each loop carries only its own path.
 template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                             const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
                                             int total, int lane, int& npos, uint32_t& cnt) {
-  const bool lane_seg = lane < nseg;
-  const bool fast = kSb && total <= 32 * kSbWords;  // warp-uniform
-  int cbase = 0;                             // fast path: segments starting before the window
-  int4 v[kW];
-  uint32_t vm[kW];
-  load_windows<kW, kSb>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, 0, cbase, v, vm);
-  for (int base = 0; base < total; base += 32 * kW) {
-    if (kPipe) {
-    int4 nv[kW];
-    uint32_t nvm[kW];
-    const int nb = base + 32 * kW;
-    if (nb < total) {
-      load_windows<kW, kSb>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, nb, cbase, nv, nvm);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kW; ++k) {
-        nvm[k] = 0;
-        nv[k] = make_int4(0, 0, 0, 0);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
-    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
-#pragma unroll
-    for (int k = 0; k < kW; ++k) {
-      v[k] = nv[k];
-      vm[k] = nvm[k];
-    }
-    } else {
-#pragma unroll
-    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
-    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
-    if (base + 32 * kW < total)
-      load_windows<kW, kSb>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, base + 32 * kW, cbase, v, vm);
-    }
-  }
+#if TCB_FASTSPLIT
+  if (kSb && total <= 32 * kSbWords)  // warp-uniform
+    probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt);
+  else
+    probe_loop<kKind, kLw, kCap, kW, false, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt);
+#else
+  probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt,
+                                               kSb && total <= 32 * kSbWords);
+#endif
 }
 
 // One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner;
@@ -449,9 +473,9 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   if (lane < nseg) {
 #if TCB_SEGPTR
     const unsigned long long p = (unsigned long long)pool + 16ll * (long long)delta;  // chunk 0 of the flat space
-    segtab[lane] = make_int4((int)(unsigned)p, (int)(unsigned)(p >> 32), excl, (incl << 8) | (lm << 4) | fm);
+    segtab[lane] = make_int4((int)(unsigned)p, (int)(unsigned)(p >> 32), excl, ((incl - 1) << 8) | (lm << 4) | fm);
 #else
-    segtab[lane] = make_int4(delta, 0, excl, (incl << 8) | (lm << 4) | fm);
+    segtab[lane] = make_int4(delta, 0, excl, ((incl - 1) << 8) | (lm << 4) | fm);
 #endif
     if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
   }
@@ -605,7 +629,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
   const int lane = threadIdx.x & 31;
   WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
   int4* segtab = segtabs[threadIdx.x >> 5];
-  reinterpret_cast<uint32_t*>(segtab + 32)[lane] = 0;  // start bitmap (kSbWords == 32)
+  for (int i = lane; i < kSbWords; i += 32) reinterpret_cast<uint32_t*>(segtab + 32)[i] = 0;  // start bitmap
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
   for (int i = lane; i < (1 << kLw); i += 32) sl.bm[i] = 0;
@@ -694,7 +718,7 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kBigWarps;
   const int nch = *a.nchunks;
   for (int i = threadIdx.x; i < (1 << kLwBig); i += kBigThreads) bm[i] = 0;
-  reinterpret_cast<uint32_t*>(segtab + 32)[lane] = 0;  // start bitmap (kSbWords == 32)
+  for (int i = lane; i < kSbWords; i += 32) reinterpret_cast<uint32_t*>(segtab + 32)[i] = 0;  // start bitmap
   Acc acc;
   int64_t staged = -1;  // node whose table is staged
   const int32_t* staged_list = nullptr;
