@@ -15,5 +15,9 @@ python tools/launch_summary.py $O/launches.csv "python bench.py --steps 5 --warm
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_engine -c 1 -o $O/engine_cfg2 -f \
     python tools/prof_count.py --config cfg2 --reps 2 > $O/ncu_full.log 2>&1
 python tools/ncu_summary.py $O/engine_cfg2.ncu-rep sass > $O/ncu_engine_cfg2.txt 2>&1
-timeout 1500 python tools/quick_perf.py --configs cfg1,cfg2,cfg3,cfg5,cfg4 > $O/engine_configs.txt 2>&1
+python tools/ncu_json.py $O/engine_cfg2.ncu-rep $O/ncu_engine_cfg2.json "ncu --set full --clock-control none --import-source on -k regex:k_engine, tools/prof_count.py (cfg2), $TAG" > /dev/null 2>&1
+timeout 300 python tools/e2e_timeline.py > $O/e2e_timeline_cfg2.txt 2>&1
+timeout 300 python tools/e2e_kernels.py > $O/e2e_kernels_cfg2.txt 2>&1
+timeout 600 python tools/rank_step.py --config cfg2 --modes replicated --ranks 2,4,8 > $O/rank_step_cfg2.txt 2>&1
+timeout 1500 python tools/quick_perf.py --configs cfg1,cfg2,cfg3,cfg5,cfg4 --no-tiled > $O/engine_configs.txt 2>&1
 echo done
