@@ -195,10 +195,11 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
 int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host, double* tier_ms_host);
 
 /* Engine tier caps (testing / tuning): key 0 = small warp-tier table cap
- * (0..256, default 256), key 2 = mid warp-tier cap (0..512, default 512),
+ * (0..128, default 128), key 2 = mid warp-tier cap (0..512, default 512),
  * key 1 = block-tier staged-table cap (0..4096, default 4096; larger tables
- * use binary search in global memory), key 3 = pairs per chunk of
- * tc_normalize_host's copy pipeline (>= 1, default 2^22; at most 16 chunks). */
+ * use binary search in global memory); value -1 restores a cap's default.
+ * key 3 = pairs per chunk of tc_normalize_host's copy pipeline (>= 1,
+ * default 2^22; at most 16 chunks). */
 int tc_set_tuning(int32_t key, int64_t value);
 
 /* |a ∩ b| of two strictly ascending int32 lists (_kernels.py:15-37). */

@@ -14,8 +14,10 @@
 //
 // Three tiers by table size d (the shape bucketing of SURVEY.md §7 step 6);
 // each tier runs over a compacted list of its own owners:
-//   small  (d <= 256): a warp owns a 4 KB shared slice -- 16K-bit hashed
-//          filter + bucketized hash table (2^7 buckets of 4 ids);
+//   small  (d <= 128): a warp owns a 2 KB shared slice -- 8K-bit hashed
+//          filter + bucketized hash table (2^6 buckets of 4 ids) -- and a
+//          4-stage ring its window loads land in by cp.async, so three
+//          windows per warp are in flight without holding registers;
 //   mid    (d <= 512): the same with 8 KB slices (4 warps per block);
 //   block  (d  > 512): a 512-thread block stages up to 4096 ids (256K-bit
 //          filter + 2^11 buckets) and all 16 warps stream the owner's
@@ -65,9 +67,9 @@ namespace tcb {
 static constexpr int kWarps = 8;          // warps per block (small tier)
 static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
-static constexpr int kTabCap = 256;       // small tier: ids per table
-static constexpr int kLwWarp = 9;         // small tier filter: 2^9 words = 16K bits (2 KB)
-static constexpr int kLbWarp = 7;         // small tier buckets: 2^7 x 4 ids (2 KB), load <= 1/2
+static constexpr int kTabCap = 128;       // small tier: ids per table
+static constexpr int kLwWarp = 8;         // small tier filter: 2^8 words = 8K bits (1 KB)
+static constexpr int kLbWarp = 6;         // small tier buckets: 2^6 x 4 ids (1 KB), load <= 1/2
 static constexpr int kMidCap = 512;       // mid tier: ids per table
 static constexpr int kLwMid = 10;         // mid tier filter: 2^10 words = 32K bits (4 KB)
 static constexpr int kLbMid = 8;          // mid tier buckets: 2^8 x 4 ids (4 KB), load <= 1/2
@@ -408,12 +410,94 @@ __device__ __forceinline__ void probe_loop(const int4* __restrict__ pool4, const
   }
 }
 
+// Asynchronous window staging (tiny tier): lane j of window b copies chunk
+// b + j into a shared-memory ring slot with cp.async (16 B, L1 bypassed)
+// and later probes it from there, so kS - 1 windows per warp are in flight
+// without holding their data in registers.  Each lane reads back only what
+// it copied itself, so the per-thread cp.async.wait_group is the only
+// synchronisation.  Returns the window's id mask for this lane (the 4-bit
+// masks of the in-flight windows ride in one register).
+template <bool kMayFast>
+__device__ __forceinline__ uint32_t issue_window(bool lane_seg, int excl, const int4* __restrict__ segtab,
+                                                 const uint32_t* __restrict__ sbits, int total, int lane,
+                                                 bool fast_rt, int b, int& cbase, int4* dst) {
+  const unsigned FULL = 0xffffffffu;
+  const bool fast = kMayFast && fast_rt;
+  int sj;
+  if (fast) {
+    const unsigned starts = sbits[b >> 5];
+    sj = cbase + __popc(starts & ((2u << lane) - 1u)) - 1;
+    cbase += __popc(starts);
+  } else {
+    const unsigned cov = __ballot_sync(FULL, lane_seg && excl <= b);
+    const unsigned bit = (lane_seg && excl > b && excl < b + 32) ? (1u << (excl - b)) : 0u;
+    const unsigned starts = __reduce_or_sync(FULL, bit);
+    sj = __popc(cov) - 1 + __popc(starts & ((2u << lane) - 1u));
+  }
+  const int f = b + lane;
+  if (f >= total) return 0u;
+  const int4 q = segtab[sj];
+  const int4* p = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(p + f) : "memory");
+  uint32_t mk = 0xFu;
+  if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
+  if (f == (q.w >> 8)) mk &= ((uint32_t)q.w >> 4) & 0xFu;
+  return mk;
+}
+
+template <int kN>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(kN) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int kKind, int kLw, int kCap, int kS, bool kMayFast>
+__device__ __forceinline__ void probe_loop_async(const Table& t, int nseg, int excl, const int4* __restrict__ segtab,
+                                                 const uint32_t* __restrict__ sbits, int total, int lane, int& npos,
+                                                 uint32_t& cnt, bool fast, int4* ring) {
+  static_assert(kS >= 2 && kS <= 8 && (kS & (kS - 1)) == 0, "ring stages: 2, 4 or 8");
+  const bool lane_seg = lane < nseg;
+  const int nwin = (total + 31) >> 5;
+  int cbase = 0;
+  uint32_t mring = 0;
+#pragma unroll
+  for (int i = 0; i < kS - 1; ++i) {
+    if (i < nwin) {
+      const uint32_t m = issue_window<kMayFast>(lane_seg, excl, segtab, sbits, total, lane, fast, 32 * i, cbase,
+                                                ring + i * 32 + lane);
+      mring |= m << (4 * i);
+    }
+    cp_async_commit();
+  }
+  for (int w = 0; w < nwin; ++w) {
+    const int wi = w + kS - 1;
+    if (wi < nwin) {
+      const int sl = wi & (kS - 1);
+      const uint32_t m = issue_window<kMayFast>(lane_seg, excl, segtab, sbits, total, lane, fast, 32 * wi, cbase,
+                                                ring + sl * 32 + lane);
+      mring = (mring & ~(0xFu << (4 * sl))) | (m << (4 * sl));
+    }
+    cp_async_commit();
+    cp_async_wait<kS - 1>();
+    const int sl = w & (kS - 1);
+    const int4 v = ring[sl * 32 + lane];
+    probe4<kKind, kLw, kCap>(t, v, (mring >> (4 * sl)) & 0xFu, lane, npos, cnt);
+    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+  }
+}
+
 // The segment resolution path (start bitmap or ballot) is chosen once per
 // group, so each loop carries only its own path.
-template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false>
+template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false, int kS = 0>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                             const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
-                                            int total, int lane, int& npos, uint32_t& cnt) {
+                                            int total, int lane, int& npos, uint32_t& cnt, int4* ring = nullptr) {
+  if (kS > 0) {
+    probe_loop_async<kKind, kLw, kCap, (kS > 0 ? kS : 2), kSb>(t, nseg, excl, segtab, sbits, total, lane, npos, cnt,
+                                                              kSb && total <= 32 * kSbWords, ring);
+    return;
+  }
 #if TCB_FASTSPLIT
   if (kSb && total <= 32 * kSbWords)  // warp-uniform
     probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt);
@@ -430,10 +514,11 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 // entries followed by the bitmap of segment starts over the group's chunks.
 // kSb: use the start bitmap (warp tiers; hub groups of the block tier are
 // mostly longer than 1024 chunks and keep the ballot/redux resolution).
-template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false>
+template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false,
+          int kS = 0>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int g0, int g1, int lane, int& npos, uint32_t& cnt,
-                                             int4* segtab, int pf_end = 0) {
+                                             int4* segtab, int pf_end = 0, int4* ring = nullptr) {
   const unsigned FULL = 0xffffffffu;
   int s = 0, e = 0;
   if (g0 + lane < g1) segs.get(g0 + lane, s, e);
@@ -483,8 +568,8 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
 #if TCB_PF_NEXT
   for (int c = s2 & ~31; c < e2; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pool + c));
 #endif
-  probe_group<kKind, kLw, kCap, kW, kSb, kPipe>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab, sbits,
-                                                total, lane, npos, cnt);
+  probe_group<kKind, kLw, kCap, kW, kSb, kPipe, kS>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab,
+                                                    sbits, total, lane, npos, cnt, ring);
   if (fast) {
     __syncwarp();
     if (lane < nseg) sbits[excl >> 5] = 0;
@@ -622,13 +707,15 @@ struct Acc {
 
 // Warp tiers (small: d <= 256 in 3 KB slices, 8 warps/block; mid:
 // d <= 1024 in 8 KB slices, 4 warps/block): each warp owns a private slice.
-template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW, bool kPipe>
+template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW, bool kPipe, int kS = 0>
 __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
   __shared__ int4 segtabs[kWPB][kSegTab];
+  __shared__ int4 rings[kWPB][kS > 0 ? kS * 32 : 1];  // cp.async window ring (kS > 0)
   const int lane = threadIdx.x & 31;
   WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
   int4* segtab = segtabs[threadIdx.x >> 5];
+  int4* ring = rings[threadIdx.x >> 5];
   for (int i = lane; i < kSbWords; i += 32) reinterpret_cast<uint32_t*>(segtab + 32)[i] = 0;  // start bitmap
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
@@ -669,8 +756,8 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         Table t{sl.bm, nullptr, nullptr, nullptr, d, 0, tlo, 0, 0, span};
         int npos = 0;
         for (int g = ra; g < rb; g += 32)
-          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
-                                                                    lane, npos, acc.cnt, segtab, rb + so);
+          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe, kS>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+                                                                        lane, npos, acc.cnt, segtab, rb + so, ring);
         __syncwarp();
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
         __syncwarp();
@@ -690,8 +777,8 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       __syncwarp();
       int npos = 0;
       for (int g = ra; g < rb; g += 32)
-        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
-                                                                   lane, npos, acc.cnt, segtab, rb + so);
+        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe, kS>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+                                                                       lane, npos, acc.cnt, segtab, rb + so, ring);
       __syncwarp();
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
       __syncwarp();
@@ -919,7 +1006,11 @@ static long long g_engine_launches = 0;
 #ifndef TCB_SMALL_PIPE
 #define TCB_SMALL_PIPE 0
 #endif
-#define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin, TCB_SMALL_PIPE>
+#ifndef TCB_SMALL_STAGES
+#define TCB_SMALL_STAGES 4
+#endif
+// small tier: 1.5 KB table slices + a 4-stage cp.async window ring per warp
+#define K_SMALL(S) k_engine<S, kLbWarp, kLwWarp, kWarps, TCB_MINBLOCKS, kWin, TCB_SMALL_PIPE, TCB_SMALL_STAGES>
 #ifndef TCB_MID_MINB
 #define TCB_MID_MINB 6
 #endif
@@ -1488,13 +1579,17 @@ int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_
 
 int tc_set_tuning(int32_t key, int64_t value) {
   return tcb::guarded([&] {
+    // value -1 restores a cap's default
     if (key == 0) {
+      if (value == -1) value = tcb::kTabCap;
       TC_REQUIRE(value >= 0 && value <= tcb::kTabCap, TC_EINVAL, "warp cap out of range");
       tcb::g_warp_cap = (int)value;
     } else if (key == 2) {
+      if (value == -1) value = tcb::kMidCap;
       TC_REQUIRE(value >= 0 && value <= tcb::kMidCap, TC_EINVAL, "mid cap out of range");
       tcb::g_mid_cap = (int)value;
     } else if (key == 1) {
+      if (value == -1) value = tcb::kBigCap;
       TC_REQUIRE(value >= 0 && value <= tcb::kBigCap, TC_EINVAL, "block cap out of range");
       tcb::g_big_cap = (int)value;
     } else if (key == 3) {

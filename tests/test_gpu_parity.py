@@ -339,9 +339,9 @@ def test_engine_tiers_forced(caps):
             for parts in (2, 3):
                 assert sum(int(count_middle_part(g, p, parts).item()) for p in range(parts)) == T, (name, parts)
     finally:
-        L.tc_set_tuning(0, 256)
-        L.tc_set_tuning(2, 512)
-        L.tc_set_tuning(1, 4096)
+        L.tc_set_tuning(0, -1)
+        L.tc_set_tuning(2, -1)
+        L.tc_set_tuning(1, -1)
 
 
 def test_dense_core_block_tier():

@@ -28,9 +28,9 @@ for caps in ((256, 512, 4096), (0, 512, 4096), (8, 16, 4096), (8, 16, 8)):
         assert int(count_lowest(g).item()) == T
         total, _ = tcb.count_space_surrogate(g, 3)
         assert total == T
-_lib.check(L.tc_set_tuning(0, 256))
-_lib.check(L.tc_set_tuning(2, 512))
-_lib.check(L.tc_set_tuning(1, 4096))
+_lib.check(L.tc_set_tuning(0, -1))
+_lib.check(L.tc_set_tuning(2, -1))
+_lib.check(L.tc_set_tuning(1, -1))
 for g in graphs:
     total, _ = emulate_ranks(g, 4)
     tcb.count_dynamic(g, 5)
