@@ -49,6 +49,9 @@ namespace tcb {
 #ifndef TCB_PF_NEXT
 #define TCB_PF_NEXT 0
 #endif
+#ifndef TCB_BIG_SB
+#define TCB_BIG_SB false
+#endif
 #ifndef TCB_BIG_PIPE
 #define TCB_BIG_PIPE 0
 #endif
@@ -67,9 +70,14 @@ namespace tcb {
 static constexpr int kWarps = 8;          // warps per block (small tier)
 static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
-static constexpr int kTabCap = 128;       // small tier: ids per table
-static constexpr int kLwWarp = 8;         // small tier filter: 2^8 words = 8K bits (1 KB)
-static constexpr int kLbWarp = 6;         // small tier buckets: 2^6 x 4 ids (1 KB), load <= 1/2
+#ifndef TCB_SMALL_CAP
+#define TCB_SMALL_CAP 128
+#define TCB_SMALL_LW 8
+#define TCB_SMALL_LB 6
+#endif
+static constexpr int kTabCap = TCB_SMALL_CAP;  // small tier: ids per table
+static constexpr int kLwWarp = TCB_SMALL_LW;   // small tier filter: 2^8 words = 8K bits (1 KB)
+static constexpr int kLbWarp = TCB_SMALL_LB;   // small tier buckets: 2^6 x 4 ids (1 KB), load <= 1/2
 static constexpr int kMidCap = 512;       // mid tier: ids per table
 static constexpr int kLwMid = 10;         // mid tier filter: 2^10 words = 32K bits (4 KB)
 static constexpr int kLbMid = 8;          // mid tier buckets: 2^8 x 4 ids (4 KB), load <= 1/2
@@ -885,10 +893,10 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           const int g = ra + 32 * gi;
           if (g >= rb) break;
           if (staged_exact)
-            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
+            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                          acc.cnt, segtab);
           else
-            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
+            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                            acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
@@ -1014,7 +1022,10 @@ static long long g_engine_launches = 0;
 #ifndef TCB_MID_MINB
 #define TCB_MID_MINB 6
 #endif
-#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE>
+#ifndef TCB_MID_STAGES
+#define TCB_MID_STAGES 0
+#endif
+#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE, TCB_MID_STAGES>
 
 struct TierShape {
   int blocks[3];   // persistent grid per tier
