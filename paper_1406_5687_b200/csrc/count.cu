@@ -276,7 +276,7 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
       // never set (span < 32 << lw keeps that word inside the bitmap)
       const uint32_t off = min((uint32_t)(xs[k] - t.tmin), t.span);
       const uint32_t wd = t.bm[off >> 5];
-      m |= ((wd >> (off & 31)) & 1u) << k;
+      m |= __funnelshift_r(wd, wd, off - k) & (1u << k);  // bit (off mod 32) rotated to position k
     }
     cnt += __popc(m & vmask);
     return;
