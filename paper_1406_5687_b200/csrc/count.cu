@@ -49,6 +49,10 @@ namespace tcb {
 #ifndef TCB_PF_NEXT
 #define TCB_PF_NEXT 0
 #endif
+#ifndef TCB_BIG_CLAIM
+#define TCB_BIG_CLAIM 16
+#endif
+static constexpr int kBigClaim = TCB_BIG_CLAIM;  // block tier: segments per dynamic claim (<= 32)
 #ifndef TCB_BIG_SB
 #define TCB_BIG_SB false
 #endif
@@ -890,14 +894,17 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           int gi = 0;
           if (lane == 0) gi = atomicAdd(&s_next, 1);
           gi = __shfl_sync(0xffffffffu, gi, 0);
-          const int g = ra + 32 * gi;
+          // kBigClaim segments per claim: hub suffixes are long (R-MAT: ~50
+          // chunks each), so a claim of a few segments is still many windows,
+          // and the wait at the next block barrier is at most one claim long
+          const int g = ra + kBigClaim * gi;
           if (g >= rb) break;
           if (staged_exact)
-            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
-                                         acc.cnt, segtab);
+            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(
+                segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
           else
-            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
-                                           acc.cnt, segtab);
+            stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(
+                segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
       } else {
@@ -1048,7 +1055,7 @@ static const TierShape& tier_shape() {
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine_big<PullSegs>, kBigThreads, kBigSmem));
     ts.blocks[2] = std::max(per_sm, 1) * sm_count();
 #ifndef TCB_BIG_WORKERS_X4
-#define TCB_BIG_WORKERS_X4 4
+#define TCB_BIG_WORKERS_X4 8
 #endif
     ts.workers[2] = std::max(1, ts.blocks[2] * TCB_BIG_WORKERS_X4 / 4);
     init = true;
