@@ -19,7 +19,7 @@ for raw in (er_edges(3000, 40000, 1), rmat_edges(11, 8, 2)):
     graphs.append(tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw))))
 core = [(a, b) for a in range(300) for b in range(a + 1, 300)]
 graphs.append(tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(core))))
-for caps in ((256, 512, 4096), (0, 512, 4096), (8, 16, 4096), (8, 16, 8)):
+for caps in ((128, 512, 4096), (0, 512, 4096), (8, 16, 4096), (8, 16, 8)):
     _lib.check(L.tc_set_tuning(0, caps[0]))
     _lib.check(L.tc_set_tuning(2, caps[1]))
     _lib.check(L.tc_set_tuning(1, caps[2]))
