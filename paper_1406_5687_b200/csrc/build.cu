@@ -683,14 +683,6 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   TC_REQUIRE(((uintptr_t)dev & 7) == 0, TC_EINVAL, "edges must be 8-byte aligned");
   Scratch sc(s);
   const int sms = sm_count();
-  const int64_t cap = std::min<int64_t>(2 * m_raw + 1, INT32_MAX);
-  uint32_t* fp = sc.alloc<uint32_t>(cap);
-  int* mm = sc.alloc<int>(3);  // min, max, label >= cap seen
-  static const int init[3] = {INT_MAX, INT_MIN, 0};
-  TC_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
-  TC_CUDA(cudaMemsetAsync(fp, 0xFF, cap * sizeof(uint32_t), s));
-  if (deg) TC_CUDA(cudaMemsetAsync(deg, 0, cap * sizeof(int32_t), s));
-
   cudaStream_t cs = copy_stream();
   constexpr int kMaxChunks = 16;
   static cudaEvent_t ev[64][kMaxChunks + 1] = {};
@@ -698,10 +690,19 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   TC_CUDA(cudaGetDevice(&d));
   if (!ev[d][0])
     for (auto& e : ev[d]) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // the copy waits only for the caller's prior work on s (dev is the
+  // caller's), not for the table initialisation below
+  TC_CUDA(cudaEventRecord(ev[d][kMaxChunks], s));
+  TC_CUDA(cudaStreamWaitEvent(cs, ev[d][kMaxChunks], 0));
+  const int64_t cap = std::min<int64_t>(2 * m_raw + 1, INT32_MAX);
+  uint32_t* fp = sc.alloc<uint32_t>(cap);
+  int* mm = sc.alloc<int>(3);  // min, max, label >= cap seen
+  static const int init[3] = {INT_MAX, INT_MIN, 0};
+  TC_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  TC_CUDA(cudaMemsetAsync(fp, 0xFF, cap * sizeof(uint32_t), s));
+  if (deg) TC_CUDA(cudaMemsetAsync(deg, 0, cap * sizeof(int32_t), s));
   const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxChunks, m_raw / g_host_chunk));
   const int64_t per = (m_raw + nch - 1) / nch;
-  TC_CUDA(cudaEventRecord(ev[d][kMaxChunks], s));  // dev is the caller's, ordered on s
-  TC_CUDA(cudaStreamWaitEvent(cs, ev[d][kMaxChunks], 0));
   for (int c = 0; c < nch; ++c) {
     const int64_t o = c * per, mc = std::min(per, m_raw - o);
     if (mc <= 0) break;
