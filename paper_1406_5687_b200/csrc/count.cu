@@ -65,9 +65,6 @@ static constexpr int kBigClaim = TCB_BIG_CLAIM;  // block tier: segments per dyn
 #ifndef TCB_SEGPTR
 #define TCB_SEGPTR 1
 #endif
-#ifndef TCB_FASTSPLIT
-#define TCB_FASTSPLIT 0
-#endif
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
@@ -499,26 +496,20 @@ __device__ __forceinline__ void probe_loop_async(const Table& t, int nseg, int e
   }
 }
 
-// The segment resolution path (start bitmap or ballot) is chosen once per
-// group, so each loop carries only its own path.
-template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false, int kS = 0>
+// kSbW: words of the warp's start bitmap (groups of <= 32 kSbW chunks take
+// the bitmap path).
+template <int kKind, int kLw, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false, int kS = 0,
+          int kSbW = kSbWords>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                             const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
                                             int total, int lane, int& npos, uint32_t& cnt, int4* ring = nullptr) {
+  const bool fast = kSb && total <= 32 * kSbW;  // warp-uniform
   if (kS > 0) {
     probe_loop_async<kKind, kLw, kCap, (kS > 0 ? kS : 2), kSb>(t, nseg, excl, segtab, sbits, total, lane, npos, cnt,
-                                                              kSb && total <= 32 * kSbWords, ring);
+                                                              fast, ring);
     return;
   }
-#if TCB_FASTSPLIT
-  if (kSb && total <= 32 * kSbWords)  // warp-uniform
-    probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt);
-  else
-    probe_loop<kKind, kLw, kCap, kW, false, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt);
-#else
-  probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt,
-                                               kSb && total <= 32 * kSbWords);
-#endif
+  probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt, fast);
 }
 
 // One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner;
@@ -527,7 +518,7 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 // kSb: use the start bitmap (warp tiers; hub groups of the block tier are
 // mostly longer than 1024 chunks and keep the ballot/redux resolution).
 template <int kKind, int kLw, class Segs, int kCap = kTabCap, int kW = kWin, bool kSb = true, bool kPipe = false,
-          int kS = 0>
+          int kS = 0, int kSbW = kSbWords>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int g0, int g1, int lane, int& npos, uint32_t& cnt,
                                              int4* segtab, int pf_end = 0, int4* ring = nullptr) {
@@ -565,7 +556,7 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   const int excl = incl - nch;
   const int delta = c0s - excl;  // chunk f of the segment is pool4[delta + f]
   uint32_t* sbits = reinterpret_cast<uint32_t*>(segtab + 32);
-  const bool fast = kSb && total <= 32 * kSbWords;
+  const bool fast = kSb && total <= 32 * kSbW;
   __syncwarp();  // the previous group's reads of segtab are done
   if (lane < nseg) {
 #if TCB_SEGPTR
@@ -580,7 +571,7 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
 #if TCB_PF_NEXT
   for (int c = s2 & ~31; c < e2; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pool + c));
 #endif
-  probe_group<kKind, kLw, kCap, kW, kSb, kPipe, kS>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab,
+  probe_group<kKind, kLw, kCap, kW, kSb, kPipe, kS, kSbW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab,
                                                     sbits, total, lane, npos, cnt, ring);
   if (fast) {
     __syncwarp();
@@ -719,16 +710,16 @@ struct Acc {
 
 // Warp tiers (small: d <= 256 in 3 KB slices, 8 warps/block; mid:
 // d <= 1024 in 8 KB slices, 4 warps/block): each warp owns a private slice.
-template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW, bool kPipe, int kS = 0>
+template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW, bool kPipe, int kS = 0, int kSbW = kSbWords>
 __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
-  __shared__ int4 segtabs[kWPB][kSegTab];
+  __shared__ int4 segtabs[kWPB][32 + kSbW / 4];
   __shared__ int4 rings[kWPB][kS > 0 ? kS * 32 : 1];  // cp.async window ring (kS > 0)
   const int lane = threadIdx.x & 31;
   WarpSliceT<kLb, kLw>& sl = slices[threadIdx.x >> 5];
   int4* segtab = segtabs[threadIdx.x >> 5];
   int4* ring = rings[threadIdx.x >> 5];
-  for (int i = lane; i < kSbWords; i += 32) reinterpret_cast<uint32_t*>(segtab + 32)[i] = 0;  // start bitmap
+  for (int i = lane; i < kSbW; i += 32) reinterpret_cast<uint32_t*>(segtab + 32)[i] = 0;  // start bitmap
   const unsigned FULL = 0xffffffffu;
   const int nch = *a.nchunks;
   for (int i = lane; i < (1 << kLw); i += 32) sl.bm[i] = 0;
@@ -768,7 +759,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         Table t{sl.bm, nullptr, nullptr, nullptr, d, 0, tlo, 0, 0, span};
         int npos = 0;
         for (int g = ra; g < rb; g += 32)
-          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe, kS>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+          stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
                                                                         lane, npos, acc.cnt, segtab, rb + so, ring);
         __syncwarp();
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
@@ -789,7 +780,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       __syncwarp();
       int npos = 0;
       for (int g = ra; g < rb; g += 32)
-        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe, kS>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
+        stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
                                                                        lane, npos, acc.cnt, segtab, rb + so, ring);
       __syncwarp();
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
@@ -1032,7 +1023,11 @@ static long long g_engine_launches = 0;
 #ifndef TCB_MID_STAGES
 #define TCB_MID_STAGES 0
 #endif
-#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE, TCB_MID_STAGES>
+#ifndef TCB_MID_SBW
+#define TCB_MID_SBW 96
+#endif
+#define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE, TCB_MID_STAGES, \
+                          TCB_MID_SBW>
 
 struct TierShape {
   int blocks[3];   // persistent grid per tier
