@@ -53,6 +53,10 @@ namespace tcb {
 #define TCB_BIG_CLAIM 16
 #endif
 static constexpr int kBigClaim = TCB_BIG_CLAIM;  // block tier: segments per dynamic claim (<= 32)
+#ifndef TCB_BIG_STAGES
+#define TCB_BIG_STAGES 0
+#endif
+static constexpr int kBigStages = TCB_BIG_STAGES;  // block tier, exact tables: cp.async ring stages per warp
 #ifndef TCB_BIG_SB
 #define TCB_BIG_SB false
 #endif
@@ -108,6 +112,8 @@ static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a
 static constexpr int kSbWords = TCB_SBWORDS;  // per-warp bitmap of segment starts: groups of <= 32 kSbWords chunks
 static constexpr int kSegTab = 32 + kSbWords / 4;  // int4 per warp: 32 segment entries + the start bitmap
 
+static_assert(kBigStages == 0 || (1 << kLbBig) >= kBigWarps * kBigStages * 32,
+              "block-tier rings live in the bucket area");
 static constexpr size_t kBigSmem = (sizeof(uint32_t) << kLwBig) + (sizeof(int4) << kLbBig) +
                                    sizeof(int32_t) * kPosCap * kBigWarps + sizeof(int4) * kSegTab * kBigWarps;
 static constexpr int kSegCost = 2;        // must match build.cu
@@ -891,8 +897,11 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           const int g = ra + kBigClaim * gi;
           if (g >= rb) break;
           if (staged_exact)
-            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(
-                segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
+            // exact tables leave the bucket area free: it holds the warps'
+            // cp.async window rings (kBigStages stages of 32 chunks each)
+            stream_group<kExact, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE, kBigStages>(
+                segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab, 0,
+                bkt + warp * (kBigStages > 0 ? kBigStages * 32 : 0));
           else
             stream_group<kBuckets, kLwBig, Segs, kTabCap, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(
                 segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
