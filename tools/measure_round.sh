@@ -21,3 +21,10 @@ timeout 300 python tools/e2e_kernels.py > $O/e2e_kernels_cfg2.txt 2>&1
 timeout 600 python tools/rank_step.py --config cfg2 --modes replicated --ranks 2,4,8 > $O/rank_step_cfg2.txt 2>&1
 timeout 1500 python tools/quick_perf.py --configs cfg1,cfg2,cfg3,cfg5,cfg4 --no-tiled > $O/engine_configs.txt 2>&1
 echo done
+# engine DRAM bandwidth on the large configs (one count each: the three tiers)
+for c in cfg3 cfg5 cfg4; do
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_engine -c 3 -o $O/engine_$c -f \
+      python tools/prof_count.py --config $c --reps 1 > $O/ncu_$c.log 2>&1
+  python tools/ncu_summary.py $O/engine_$c.ncu-rep > $O/ncu_engine_$c.txt 2>&1
+done
+echo done-large
