@@ -69,6 +69,9 @@ static constexpr int kBigStages = TCB_BIG_STAGES;  // block tier, exact tables: 
 #ifndef TCB_SEGPTR
 #define TCB_SEGPTR 1
 #endif
+#ifndef TCB_WIPE
+#define TCB_WIPE 1
+#endif
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
@@ -689,6 +692,15 @@ __device__ __forceinline__ int advance_owner32(const EngineArgs& a, int x, int r
   }
 }
 
+// Clears a warp's filter slice: when the slice is at most 4 words per id
+// of the table, a 16-byte store per lane per 512 bytes beats re-reading and
+// re-hashing the table's ids.
+template <int kLw>
+__device__ __forceinline__ void wipe_filter(uint32_t* bm, int lane, int words = 1 << kLw) {
+  int4* b4 = reinterpret_cast<int4*>(bm);
+  for (int i = lane; i < words / 4; i += 32) b4[i] = make_int4(0, 0, 0, 0);
+}
+
 // Per-warp accumulation, flushed per bucket.
 struct Acc {
   unsigned long long acc = 0;  // same on all lanes
@@ -754,9 +766,17 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       const int32_t* gtab = a.tab_indices + ow.t0;
       const int32_t tlo = ow.tlo;
       const uint32_t span = ow.span;
-      if (span < (32u << kLw)) {
+      // exact tables use the whole slice (filter and bucket words) as the bitmap
+      constexpr int kExactWords = (1 << kLw) + 4 * (1 << kLb);
+      if (span < 32u * kExactWords) {
         // Narrow id span (hub owners at the top of the degree order): the
-        // filter words become an exact direct-mapped bitmap over [tlo, tlo+span).
+        // slice becomes an exact direct-mapped bitmap over [tlo, tlo+span).
+        // The filter words are zero between owners; the bucket words hold
+        // the last hashed owner's table and are zeroed here.
+        if (span >= 32u << kLw) {
+          for (int i = lane; i < (1 << kLb); i += 32) sl.bkt[i] = make_int4(0, 0, 0, 0);
+          __syncwarp();
+        }
         for (int i = lane; i < d; i += 32) {
           const uint32_t off = (uint32_t)(__ldg(&gtab[i]) - tlo);
           atomicOr(&sl.bm[off >> 5], 1u << (off & 31));
@@ -768,7 +788,11 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
           stream_group<kExact, kLw, Segs, kTabCap, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
                                                                         lane, npos, acc.cnt, segtab, rb + so, ring);
         __syncwarp();
+#if TCB_WIPE
+        wipe_filter<kLw + 0>(sl.bm, lane, kExactWords);
+#else
         for (int i = lane; i < d; i += 32) sl.bm[(uint32_t)(__ldg(&gtab[i]) - tlo) >> 5] = 0;
+#endif
         __syncwarp();
         continue;
       }
@@ -789,7 +813,11 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         stream_group<kInline, kLw, Segs, kTabCap, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
                                                                        lane, npos, acc.cnt, segtab, rb + so, ring);
       __syncwarp();
+#if TCB_WIPE
+      wipe_filter<kLw>(sl.bm, lane);
+#else
       for (int i = lane; i < d; i += 32) filt_clear<kLw>(sl.bm, __ldg(&gtab[i]));
+#endif
       __syncwarp();
     }
     acc.fold();
