@@ -339,7 +339,9 @@ def _gpu_arm_core(args):
             count_middle(g, out=out)
         return out
 
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    # > 126 MB L2; 1 GB also keeps the device busy (~0.2 ms) while the host
+    # enqueues the timed step, so host launch jitter cannot leak into it
+    flush = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
 
     for _ in range(args.warmup):
         count_step()
@@ -432,7 +434,7 @@ def _gpu_arm_core(args):
         "data": "synthetic (seeded generator; no dataset)",
         "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw,
                    "triangles": T, "W_succsum": W,
-                   "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 256 MB L2 flush before every timed step",
+                   "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 1 GB L2 flush before every timed step",
                    "parallelism": {"single": "1 GPU",
                                    "replicated": f"{world} GPUs, replicated graph, engine chunks interleaved across ranks + NCCL all-reduce",
                                    "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
