@@ -307,6 +307,9 @@ __global__ void k_degrees(const int64_t* __restrict__ indptr, const int32_t* __r
 // row lengths); each lane walks from the chunk's first row to its own.
 // Phased over destination rows like k_orient_scatter.
 static constexpr int kRevSpan = 1024;
+#ifndef TCB_REV_COST_STREAM
+#define TCB_REV_COST_STREAM 1
+#endif
 __global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
                               int64_t n, int64_t m, const int64_t* __restrict__ rev_indptr,
                               const int64_t* __restrict__ bounds, int ph, int32_t* cursor, int32_t* back,
@@ -448,6 +451,41 @@ __global__ void k_rev_cost(const int64_t* __restrict__ rev_indptr, const int2* _
       }
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) cost[u] = (d > 0 && r1 > r0) ? (int64_t)s + d + kTabCost : 0;
+  }
+}
+
+// Streaming form of k_rev_cost: thread t sums the suffix lengths of
+// kCostRun consecutive reverse entries (coalesced reads of the flat rev_seg
+// array), finding the row of its first entry by binary search and walking
+// row boundaries from there; each row's partial sum goes out with one
+// fire-and-forget atomic.  k_rev_cost_fin adds the per-row terms.
+static constexpr int kCostRun = 8;
+__global__ void k_rev_len_sum(const int64_t* __restrict__ rev_indptr, const int2* __restrict__ rev_seg, int64_t n,
+                              int64_t m, unsigned long long* acc) {
+  const int64_t nt = (m + kCostRun - 1) / kCostRun;
+  GRID_STRIDE(t, nt) {
+    const int64_t r0 = t * kCostRun, r1 = min(m, r0 + kCostRun);
+    int64_t u = row_of_edge(rev_indptr, n, r0);
+    int64_t uend = rev_indptr[u + 1];
+    unsigned long long s = 0;
+    for (int64_t r = r0; r < r1; ++r) {
+      while (r >= uend) {  // row change: flush (rows may be empty)
+        if (s) atomicAdd(&acc[u], s);
+        s = 0;
+        uend = rev_indptr[++u + 1];
+      }
+      const int2 sg = rev_seg[r];
+      s += (unsigned long long)(sg.y - sg.x);
+    }
+    if (s) atomicAdd(&acc[u], s);
+  }
+}
+
+__global__ void k_rev_cost_fin(const int64_t* __restrict__ rev_indptr, const int64_t* __restrict__ eff_indptr,
+                               const unsigned long long* __restrict__ acc, int64_t n, int64_t* cost) {
+  GRID_STRIDE(u, n) {
+    const int64_t d = eff_indptr[u + 1] - eff_indptr[u], k = rev_indptr[u + 1] - rev_indptr[u];
+    cost[u] = (d > 0 && k > 0) ? (int64_t)acc[u] + kSegCost * k + d + kTabCost : 0;
   }
 }
 
@@ -963,9 +1001,23 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   }
   // pull-engine cost prefix over u
   int64_t* cu = sc.alloc<int64_t>(n + 1);
+#if TCB_REV_COST_STREAM
+  {
+    auto* acc = sc.alloc<unsigned long long>(n);
+    TC_CUDA(cudaMemsetAsync(acc, 0, n * sizeof(unsigned long long), s));
+    if (m) {
+      k_rev_len_sum<<<grid_for((m + kCostRun - 1) / kCostRun, kBlock, sms * 16), kBlock, 0, s>>>(
+          rev_indptr, reinterpret_cast<const int2*>(rev_seg), n, m, acc);
+      check_launch();
+    }
+    k_rev_cost_fin<<<grid_for(n, kBlock, sms * 8), kBlock, 0, s>>>(rev_indptr, eff_indptr, acc, n, cu);
+    check_launch();
+  }
+#else
   k_rev_cost<<<grid_for(n * 32, kBlock, sms * 16), kBlock, 0, s>>>(
       rev_indptr, reinterpret_cast<const int2*>(rev_seg), eff_indptr, n, cu);
   check_launch();
+#endif
   TC_CUDA(cudaMemsetAsync(cu + n, 0, sizeof(int64_t), s));
   {
     size_t tmp = 0;
