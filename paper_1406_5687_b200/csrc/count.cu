@@ -15,10 +15,12 @@
 // Three tiers by table size d (the shape bucketing of SURVEY.md §7 step 6);
 // each tier runs over a compacted list of its own owners:
 //   small  (d <= 128): a warp owns a 2 KB shared slice -- 8K-bit hashed
-//          filter + bucketized hash table (2^6 buckets of 4 ids) -- and a
-//          4-stage ring its window loads land in by cp.async, so three
-//          windows per warp are in flight without holding registers;
-//   mid    (d <= 512): the same with 8 KB slices (4 warps per block);
+//          filter (two bits per id) + bucketized hash table (2^6 buckets of
+//          4 ids) -- and a 4-stage ring its window loads land in by
+//          cp.async, so three windows per warp are in flight without
+//          holding registers;
+//   mid    (d <= 512): 8 KB slices (32K-bit two-bit filter + 2^8 buckets),
+//          4 warps per block, windows software-pipelined in registers;
 //   block  (d  > 512): a 512-thread block stages up to 4096 ids (256K-bit
 //          filter + 2^11 buckets) and all 16 warps stream the owner's
 //          segments -- the hubs of Chung-Lu / R-MAT; beyond 4096 ids the
@@ -26,10 +28,11 @@
 // Segment streaming (all tiers): a warp takes 32 segments, compacts the
 // non-empty ones, and flattens the 16-byte chunks they touch with a warp
 // scan; lane j of a window loads chunk base+j as one int4 (4 list ids),
-// resolving its segment with one ballot + one redux.or + popc.  A probe is
-// one filter LDS and three ALU ops, branch-free over the 4 ids; only filter
-// hits are verified (one LDS.128 in the bucket table: inline in the warp
-// tiers, queued and verified in bulk in the block tier).
+// resolving its segment from a shared bitmap of segment starts (popc) or,
+// for groups wider than the bitmap, one ballot + one redux.or + popc.  A
+// probe is one filter LDS and a few ALU ops, branch-free over the 4 ids;
+// only filter hits are verified (one LDS.128 in the bucket table: inline in
+// the warp tiers, queued and verified in bulk in the block tier).
 //
 // Load balance (the paper's dynamic load balancing, PAPER.md:788-822,
 // dynamic_lb.py:68-109, restated for warps): each tier splits its owners'
@@ -158,10 +161,11 @@ struct PushSegs {  // forward edge e of v -> N^_u, u = indices[e]
   }
 };
 
-// Per-owner tables.  Every staged table has a hashed one-bit filter in
-// front (2^lw words, h = id * golden, word = h >> (32 - lw), bit =
-// (h >> (27 - lw)) & 31): a probe is one LDS.32 and three ALU ops, and only
-// filter hits (true hits plus ~d/2^(lw+5) false positives) are verified:
+// Per-owner tables.  Every staged table has a hashed filter in front (2^lw
+// words, h = id * golden, word = h >> (32 - lw), bit h & 31, and in the warp
+// tiers a second bit (h >> 5) & 31 in the same word): a probe is one LDS.32
+// and a few ALU ops, and only filter hits (true hits plus the false
+// positives: ~d/2^(lw+5) with one bit, ~20x fewer with two) are verified:
 //   kInline  (warp tiers): inline lookup in a bucketized hash table whose
 //            maximum displacement is recorded at build time, so a lookup is a
 //            warp-uniform handful of LDS.128 (usually one), no search loop;
