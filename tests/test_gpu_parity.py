@@ -390,6 +390,28 @@ def test_build_row_sort_classes():
         assert tcb.count_triangles_seq(g) == O.count_triangles(og)
 
 
+def test_build_duplicate_edges_short_rows():
+    """build_graph keeps duplicate edges (graph.py:143-153): forward
+    rows with repeated ids, ragged lengths up to ~150 (CUB's sub-warp sorts
+    and the first warp merge sort class), in both orders, against the oracle."""
+    rng = np.random.default_rng(5)
+    parts = []
+    for hub, size in enumerate((2, 3, 31, 32, 33, 64, 65, 97, 127, 128, 129)):
+        nb = rng.integers(200, 400, size=size)
+        nb[: size // 3] = nb[0]  # a run of one repeated neighbour
+        parts.append(np.stack([np.full(size, hub), nb], 1))
+    parts.append(rng.integers(0, 400, size=(3000, 2)))
+    raw = np.concatenate(parts).astype(np.int64)
+    raw = raw[raw[:, 0] != raw[:, 1]]
+    rg = tcb.RawGraph(n=400, edges=raw)
+    for order in (None, np.arange(400, dtype=np.int64)):  # identity order: the hubs' rows are long
+        og = O.build_graph(400, raw, order=order)
+        g = tcb.build_graph(rg) if order is None else G._build_graph_input_order(rg)
+        for f in ("eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg"):
+            assert np.array_equal(host(getattr(g, f)), getattr(og, f)), f
+    assert np.diff(og.eff_indptr).max() > 128
+
+
 def _host_pinned(a):
     return torch.as_tensor(np.ascontiguousarray(np.asarray(a, np.int32).reshape(-1, 2))).pin_memory()
 
