@@ -617,6 +617,41 @@ void present_labels(Scratch& sc, const uint32_t* fp, int64_t L1, int64_t* K, int
   *Lf = (int64_t)(int32_t)(uint32_t)hk[1];
 }
 
+// Census of a sorted pair list (8-byte pairs read as one word): [0] pairs
+// equal to their successor, self-loop sentinels (-1, -1) excluded; [1]
+// sentinels.
+__global__ void k_dup_census(const long long* __restrict__ e, int64_t m, unsigned long long* cnt) {
+  constexpr int U = 4;  // independent loads in flight per thread
+  unsigned long long d = 0, z = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < m; i0 += U * stride) {
+    long long a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      a[u] = i < m ? __ldg(&e[i]) : 0;
+      b[u] = i + 1 < m ? __ldg(&e[i + 1]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < m) {
+        if (a[u] == -1ll) ++z;
+        else if (i + 1 < m && b[u] == a[u]) ++d;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    z += __shfl_xor_sync(0xffffffffu, z, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (d | z)) {
+    atomicAdd(&cnt[0], d);
+    atomicAdd(&cnt[1], z);
+  }
+}
+
 // normalize from the label census on: the first-seen map, packing, sort
 // and unique (graph.py:95-103).  sorted32 (nullable): the list's keys
 // (min << 32 | max, raw labels; a self-loop as ~0, flagged by `sentinel`)
@@ -856,7 +891,39 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   present_labels(sc, fp, L1, &K, &Lf, s);
   const unsigned long long* sorted32 = nullptr;
   if (runs && K == Lf + 1) {  // join the remaining runs, smallest first
-    while (stack.size() > 1) merge_top();
+    while (stack.size() > 2) merge_top();
+    if (stack.size() == 2) {
+      // Last level straight into the output pairs; when the census finds no
+      // duplicate edge (self-loop sentinels sort last and are cut off) this
+      // is the unique list and the select pass is skipped.  Otherwise the
+      // level is merged again into keys for the unique pass.
+      const Run r1 = stack[0], r2 = stack[1];
+      auto out = thrust::make_transform_output_iterator(reinterpret_cast<int2*>(out_edges), UnpackKey{32});
+      size_t need = 0;
+      TC_CUDA(cub::DeviceMerge::MergeKeys(nullptr, need, r1.buf + r1.o, (int)r1.len, r2.buf + r2.o, (int)r2.len,
+                                          out, KeyLess(), s));
+      if (need > mcap) {
+        mws = sc.bytes(need);
+        mcap = need;
+      }
+      TC_CUDA(cub::DeviceMerge::MergeKeys(mws, need, r1.buf + r1.o, (int)r1.len, r2.buf + r2.o, (int)r2.len, out,
+                                          KeyLess(), s));
+      auto* cnt = sc.alloc<unsigned long long>(2);
+      TC_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), s));
+      k_dup_census<<<grid_for(m_raw, kBlock, sms * 16), kBlock, 0, s>>>(reinterpret_cast<const long long*>(out_edges),
+                                                                        m_raw, cnt);
+      check_launch();
+      unsigned long long hc[2];
+      TC_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      sync_stream(s);
+      if (hc[0] == 0) {
+        *m_host = m_raw - (int64_t)hc[1];
+        *n_host = K;
+        if (deg_valid) *deg_valid = (*m_host == m_raw && *n_host == L1) ? 1 : 0;
+        return;
+      }
+      merge_top();
+    }
     sorted32 = stack[0].buf;
   }
   normalize_tail(sc, dev, m_raw, fp, L1, K, Lf, out_edges, m_host, n_host, s, sorted32, any_loop);

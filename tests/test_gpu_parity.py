@@ -417,7 +417,8 @@ def _host_pinned(a):
 
 
 @pytest.mark.parametrize("chunk", [1 << 22, 100_000])
-@pytest.mark.parametrize("case", ["pa", "pa_sparse", "sorted", "dups_loops", "sparse_big", "sparse_small"])
+@pytest.mark.parametrize("case", ["pa", "pa_loops", "pa_sparse", "sorted", "dups_loops", "sparse_big",
+                                  "sparse_small"])
 def test_normalize_host_pipeline(case, chunk, monkeypatch):
     """normalize of a pinned host list (chunked H2D copy with the
     first-occurrence / degree passes and per-chunk sorted runs behind it,
@@ -431,6 +432,10 @@ def test_normalize_host_pipeline(case, chunk, monkeypatch):
     rng = np.random.default_rng(3)
     if case == "pa":  # dense labels, no self-loop or duplicate: degrees handed over
         raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy()
+    elif case == "pa_loops":  # dense, self-loops but no duplicate: the last merge level is the output
+        raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy()
+        loops = np.repeat(np.arange(0, 200_000, 997), 2).reshape(-1, 1).repeat(2, 1)
+        raw = np.insert(raw, rng.integers(0, len(raw), len(loops)), loops, axis=0)
     elif case == "pa_sparse":  # per-chunk runs, but labels not dense: first-seen map
         raw = pa_edges_host(tcb.PaParams(n=200_000, d=10, seed=4)).numpy() * 2
     elif case == "sorted":  # an already normalized list
