@@ -1,5 +1,6 @@
-mkdir -p gpurun_out/chunk
+#!/bin/bash
 # tools/chunk_sweep.sh -- e2e ms of bench.py at several host-pipeline chunk sizes (tc_set_tuning key 3; dev tool)
+mkdir -p gpurun_out/chunk
 for r in 1 2; do
 for c in 4194304 4100000 3550000 6200000 5000000; do
   timeout 300 python -c "
