@@ -228,7 +228,7 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": CONFIGS[args.config]["desc"], "n": g.n, "m": g.m},
+        "config": {"workload": CONFIGS[args.config]["desc"], "n": g.n, "m": g.m, "m_raw": int(raw.shape[0])},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -248,6 +248,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-target-s", type=float, default=12.0)
+    ap.add_argument("--other-configs", default="cfg3,cfg5,cfg4",
+                    help="N=1: also measure these BASELINE configs (engine, roofline, cold count, e2e; GPU arm "
+                         "only) into the line's other_configs; '' to skip")
     ap.add_argument("--mode", default="replicated", choices=["replicated", "surrogate", "direct"],
                     help="N>1: replicated graph, the engine's chunk plan interleaved across ranks (default), the paper's "
                          "non-overlapping partition with surrogate list exchange, or the direct scheme as a "
@@ -268,9 +271,172 @@ def run_ours(args):
     return 0
 
 
-def _gpu_arm_core(args):
+def engine_bytes(g):
+    """Algorithmic bytes of one middle-vertex engine launch over g (DESIGN.md
+    §3.2, "Roofline"): every probe id streamed once (4 B x sum_v C(d^_v, 2),
+    the suffixes of N^_v after each u), the segment coordinates of every
+    owner's predecessors (8 B each), every owner's table N^_u (4 B per id) and
+    its plan descriptor + tier row (40 B).  Returns (bytes, detail)."""
+    import torch
+
+    d = g.eff_deg.to(torch.int64)
+    probes = int((d * (d - 1) // 2).sum())
+    own = (g._rev_cost[1:] - g._rev_cost[:-1]) > 0
+    n_own = int(own.sum())
+    tab = int(d[own].sum())
+    segs = int((g._rev_indptr[1:] - g._rev_indptr[:-1])[own].sum())
+    b = 4 * probes + 8 * segs + 4 * tab + 40 * n_own
+    return b, {"probe_ids": probes, "segments": segs, "table_ids": tab, "owners": n_own}
+
+
+def _sha_file(path):
+    import hashlib
+
+    with open(path, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def ncu_traffic(cfg):
+    """DRAM bytes per engine launch from the committed ncu capture of this
+    config (profiles/ncu_engine_<cfg>.json, tools/ncu_json.py), valid only if
+    it was captured from the engine source this run executes (sha of
+    csrc/count.cu stamped in the file)."""
+    tpath = os.path.join(REPO, "profiles", f"ncu_engine_{cfg}.json")
+    src_sha = _sha_file(os.path.join(REPO, "paper_1406_5687_b200", "csrc", "count.cu"))
+    if not os.path.exists(tpath):
+        return None, f"no ncu capture for {cfg}"
+    with open(tpath) as f:
+        d = json.load(f)
+    if d.get("count_cu_sha") != src_sha:
+        return None, f"stale: {os.path.relpath(tpath, REPO)} was captured from count.cu {d.get('count_cu_sha')}, " \
+                     f"this run is {src_sha}"
+    return d.get("dram_bytes_per_launch"), f"{os.path.relpath(tpath, REPO)} ({d.get('source')}; count.cu {src_sha})"
+
+
+def roofline_of(g, cfg, engine_ms, W):
+    peak, peak_src = measured_peak()
+    b_eng, detail = engine_bytes(g)
+    achieved = b_eng / (engine_ms / 1e3) / 1e9
+    traffic, tsrc = ncu_traffic(cfg)
+    b_merge = 4 * W + 20 * g.m + 8 * (g.n + 1)
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "traffic_source": tsrc,
+            "traffic_frac": None if traffic is None else traffic / (engine_ms / 1e3) / 1e9 / peak,
+            "kernel": "middle-vertex engine (k_small / k_engine<mid> / k_engine_big tiers, one launch each)",
+            "bytes_per_launch": b_eng, "bytes_detail": detail,
+            "bytes_model": "4*sum_v C(d^_v,2) (streamed suffix ids) + 8*segments + 4*table ids + 40*owners",
+            "kernel_ms": engine_ms, "peak_source": peak_src,
+            "merge_equiv_gbs": b_merge / (engine_ms / 1e3) / 1e9,
+            "merge_equiv_note": "SURVEY §8(d) merge model 4W+20m+8(n+1) over the engine time; the engine never "
+                                "moves those bytes (it probes sum C(d^,2) ids, not W merge steps): not a bandwidth"}
+
+
+def golden_T(cfg):
+    """Reference-pinned (cfg 1, 2) or oracle (cfg 3-5) triangle totals."""
+    for name in ("configs.json", "scale.json"):
+        try:
+            with open(os.path.join(REPO, "tests", "golden", name)) as f:
+                d = json.load(f)
+        except OSError:
+            continue
+        if cfg in d and "T" in d[cfg]:
+            return int(d[cfg]["T"]), name
+    return None, None
+
+
+def _engine_ms(fn, steps, flush):
+    """Average device time of the engine launches (CUDA events on the
+    engine's stream, tc_engine_timing) over `steps` calls of fn."""
     import ctypes
 
+    import torch
+
+    from paper_1406_5687_b200 import _lib
+
+    _lib.lib().tc_engine_timing(1, None, None, None)
+    for _ in range(steps):
+        flush.fill_(1)
+        fn()
+    torch.cuda.synchronize()
+    tot, nl = ctypes.c_double(), ctypes.c_longlong()
+    tiers = (ctypes.c_double * 3)()
+    _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl), tiers)
+    k = max(1, nl.value)
+    return tot.value / k, [t / k for t in tiers]
+
+
+def _cold_count_ms(g, reps, flush):
+    """count_triangles_seq on a graph whose engine plan is not built yet:
+    plan (tier lists, chunk plan, one host read-back) + engine."""
+    import torch
+
+    import paper_1406_5687_b200 as tcb
+
+    ts = []
+    for _ in range(reps):
+        g._cache.clear()
+        flush.fill_(1)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        tcb.count_triangles_seq(g)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.median(ts)
+
+
+def other_config(cfg, steps, warmup, flush):
+    """Engine, cold count and e2e of one more BASELINE config on this GPU
+    (GPU arm only), with T checked against the committed golden total."""
+    import torch
+
+    import paper_1406_5687_b200 as tcb
+    from paper_1406_5687_b200.sequential import count_middle
+
+    t0 = time.perf_counter()
+    raw_host = host_raw_edges(cfg, pin=True)
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw_host)))
+    out = torch.empty(1, dtype=torch.int64, device=g.eff_indptr.device)
+    T = int(count_middle(g, out=out).item())
+    want, src = golden_T(cfg)
+    W = int(tcb.node_costs(g, tcb.CostKind.SUCC_SUM).sum())
+    for _ in range(warmup):
+        count_middle(g, out=out)
+    engine_ms, tier_ms = _engine_ms(lambda: count_middle(g, out=out), steps, flush)
+    cold = _cold_count_ms(g, 2, flush)
+    rl = roofline_of(g, cfg, engine_ms, W)
+    n, m, m_raw = g.n, g.m, int(raw_host.shape[0])
+    del g
+    torch.cuda.empty_cache()
+    e2e = []
+    for i in range(1 + min(steps, 3)):
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        gg = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw_host)))
+        tri = tcb.count_triangles_seq(gg)
+        e.record()
+        torch.cuda.synchronize()
+        if tri != T:
+            raise RuntimeError(f"{cfg}: e2e count mismatch")
+        if i:
+            e2e.append(s.elapsed_time(e))
+        del gg
+    torch.cuda.empty_cache()
+    log(f"[ours] {cfg}: n={n} m={m} T={T} engine {engine_ms:.2f} ms e2e {statistics.median(e2e):.1f} ms "
+        f"({time.perf_counter() - t0:.0f}s)")
+    return {"workload": CONFIGS[cfg]["desc"], "n": n, "m": m, "m_raw": m_raw, "triangles": T,
+            "triangles_golden": want, "triangles_ok": (want == T) if want is not None else None,
+            "golden_source": src, "kernel_ms": engine_ms, "tier_ms": tier_ms, "count_cold_ms": cold,
+            "edges_per_s": m / (engine_ms / 1e3), "frac": rl["frac"], "achieved_gbs": rl["achieved"],
+            "bytes_per_launch": rl["bytes_per_launch"], "traffic": rl["traffic"],
+            "traffic_frac": rl["traffic_frac"],
+            "e2e_ms": statistics.median(e2e), "e2e_edges_per_s": m / (statistics.median(e2e) / 1e3),
+            "e2e_h2d_bytes": m_raw * 8}
+
+
+def _gpu_arm_core(args):
     import torch
     import torch.distributed as dist
 
@@ -366,15 +532,13 @@ def _gpu_arm_core(args):
         raise RuntimeError("count changed between steps")
 
     # dominant kernel (the engine) timed with CUDA events on its own stream
-    _lib.lib().tc_engine_timing(1, None, None, None)
-    for _ in range(args.steps):
-        flush.fill_(1)
-        count_step()
-    torch.cuda.synchronize()
-    tot, nl = ctypes.c_double(), ctypes.c_longlong()
-    tiers = (ctypes.c_double * 3)()
-    _lib.lib().tc_engine_timing(0, ctypes.byref(tot), ctypes.byref(nl), tiers)
-    engine_ms = max_over_ranks(tot.value / max(1, nl.value))
+    engine_ms, tier_ms = _engine_ms(count_step, args.steps, flush)
+    engine_ms = max_over_ranks(engine_ms)
+    cold_ms = None
+    if mode == "single":
+        cold_ms = _cold_count_ms(g, 3, flush)
+    rl = roofline_of(g, args.config, engine_ms, W) if rank == 0 else None
+    want, gsrc = golden_T(args.config)
 
     e2e_ms = None
     if not args.no_e2e:
@@ -406,8 +570,18 @@ def _gpu_arm_core(args):
                 samples.append(s.elapsed_time(e))
             del gg
         e2e_ms = max_over_ranks(sum(samples) / len(samples))
+    else:
+        del g
+    torch.cuda.empty_cache()
 
     clock_summary = clocks.summary()
+    others = []
+    if rank == 0 and world == 1 and args.other_configs:
+        for oc in [c for c in args.other_configs.split(",") if c and c != args.config]:
+            try:
+                others.append(other_config(oc, max(3, min(args.steps, 5)), 2, flush))
+            except Exception as exc:  # reported, never required
+                others.append({"workload": oc, "error": repr(exc)})
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -419,39 +593,35 @@ def _gpu_arm_core(args):
     if rank != 0:
         return None
 
-    peak, peak_src = measured_peak()
-    b_alg = 4 * W + 20 * m + 8 * (n + 1)
-    achieved = b_alg / (engine_ms / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", f"ncu_engine_{args.config}.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": m / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded generator; no dataset)",
-        "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw,
-                   "triangles": T, "W_succsum": W,
-                   "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 1 GB L2 flush before every timed step",
-                   "parallelism": {"single": "1 GPU",
-                                   "replicated": f"{world} GPUs, replicated graph, engine chunks interleaved across ranks + NCCL all-reduce",
-                                   "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
-                                                "(NCCL all-to-all) + NCCL all-reduce",
-                                   "direct": f"{world} GPUs, SUCC_SUM node-range shards, deduplicated pull of remote "
-                                             "N^_u (NCCL all-to-all) + NCCL all-reduce"}[mode]},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_engine<PullSegs> (middle-vertex engine)",
-                     "bytes_model": "B_alg = 4W + 20m + 8(n+1) per launch (SURVEY §8(d) merge model)",
-                     "kernel_ms": engine_ms, "peak_source": peak_src},
+        # identical to the reference arm's config (same workload, same graph)
+        "config": {"workload": CONFIGS[args.config]["desc"], "n": n, "m": m, "m_raw": m_raw},
+        "workload_detail": {
+            "triangles": T, "triangles_golden": want, "golden_source": gsrc, "W_succsum": W,
+            "l2": "inputs > L2 (rev_seg 8 B/edge + eff_indices) and a 1 GB L2 flush before every timed step",
+            "step": "count_triangles_seq with the graph's engine plan (tier lists, chunk plan) built at the first "
+                    "count and reused; count_cold_ms is plan + engine on a graph without one",
+            "mode": mode,
+            "parallelism": {"single": "1 GPU",
+                            "replicated": f"{world} GPUs, replicated graph, engine chunks interleaved across ranks + NCCL all-reduce",
+                            "surrogate": f"{world} GPUs, PRED_SUM node-range shards, surrogate list exchange "
+                                         "(NCCL all-to-all) + NCCL all-reduce",
+                            "direct": f"{world} GPUs, SUCC_SUM node-range shards, deduplicated pull of remote "
+                                      "N^_u (NCCL all-to-all) + NCCL all-reduce"}[mode]},
+        "count_cold_ms": cold_ms,
+        "engine_tier_ms": tier_ms,
+        "roofline": rl,
         "cpu_baseline": cpu,
         "e2e": None if e2e_ms is None else {
             "value": m / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": m_raw * 8,
             "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
             "path": "pinned host raw pairs -> normalize (chunked H2D overlapped with its first passes) -> "
                     "build_graph -> count_triangles_seq -> D2H"},
+        "other_configs": others,
         "gpu_launches": launches,
         "clocks": clock_summary,
     }

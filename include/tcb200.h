@@ -69,7 +69,9 @@ int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges,
  * *deg_valid = 1 when it is the normalized graph's degree array (dense
  * labels kept, no self-loop or duplicate dropped), for tc_build_graph_deg.
  * Replaces the H2D copy + graph.normalize of a host list (graph.py:76-103).
- * Synchronises (returns m, n). */
+ * Synchronises (returns m, n).  Calls for one device are serialised by a
+ * per-device lock (they share that device's copy stream, chunk events and
+ * mapped flag slots); calls for different devices run concurrently. */
 int tc_normalize_host(const int32_t* host_edges, int64_t m_raw, int32_t* dev_edges, int32_t* out_edges,
                       int64_t* m_host, int64_t* n_host, int32_t* deg, int32_t* deg_valid,
                       tc_stream_t stream);
@@ -132,7 +134,9 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
  * and re-plans itself if tc_set_tuning changed the tier caps.  Planning does
  * not synchronise at its end: runs wait on the plan's event (a run captured
  * into a CUDA graph must be captured after the planning stream has
- * synchronised). */
+ * synchronised).  Runs of one plan share its chunk-queue counters, so runs
+ * issued on different streams are serialised: each run waits on the event
+ * the previous run recorded behind its engine launches. */
 typedef struct tc_plan_s* tc_plan_t;
 int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
                    const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,

@@ -9,6 +9,8 @@
 #include <cub/device/device_merge.cuh>
 #include <thrust/iterator/transform_output_iterator.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace tcb {
@@ -761,6 +763,12 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   static cudaEvent_t ev[64][kMaxChunks + 1] = {};
   int d = 0;
   TC_CUDA(cudaGetDevice(&d));
+  // The copy stream, the chunk events and the mapped flag slots below are
+  // per device and shared by every call: one call per device at a time (the
+  // host waits on every chunk's flags before returning, so nothing of a
+  // call's flag traffic outlives it).
+  static std::mutex call_mu[64];
+  std::lock_guard<std::mutex> call_lock(call_mu[d]);
   if (!ev[d][0])
     for (auto& e : ev[d]) TC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // the copy waits only for the caller's prior work on s (dev is the

@@ -837,6 +837,314 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
   acc.flush(a.out, lane);
 }
 
+// ------------------------------------------------------------ small tier (v20)
+//
+// Owners with d <= 128 (cfg 2: every owner).  The v19 form of this tier was
+// bound by the SM's shared-memory data pipe (ncu, profiles/r13_*: 81% of
+// peak LSU wavefronts, 410 M shared wavefronts per launch at cfg 2): 19% went
+// to the cp.async window ring (write + read back), 14% to building a
+// bucketized hash table per owner with atomicCAS, 9% to 16-byte segment-table
+// reads.  v20 keeps only the hashed two-bit filter in shared memory and
+//   * holds the owner's list N^_u in registers (4 ids per lane, d <= 128) and
+//     verifies the rare filter hits against it with one shuffle + one ballot
+//     per hit (no bucket table to build or read);
+//   * loads the windows straight into registers with 16-byte streaming loads
+//     (ld.global.nc.L1::no_allocate), no shared-memory staging;
+//   * keeps 8-byte segment-table entries (chunk offset, last chunk | masks);
+//     whether a chunk is its segment's first comes from the start bitmap.
+#ifndef TCB_SMALL_V20
+#define TCB_SMALL_V20 1
+#endif
+#ifndef TCB_SMALL_W
+#define TCB_SMALL_W 3  // windows per step
+#endif
+#ifndef TCB_SMALL_PIPE2
+#define TCB_SMALL_PIPE2 0  // issue the next step's loads before probing the current one
+#endif
+#ifndef TCB_SMALL_MINB
+#define TCB_SMALL_MINB 5
+#endif
+#ifndef TCB_SMALL_LWS
+#define TCB_SMALL_LWS 10  // filter words = 2^10 (32K bits, 4 KB per warp); exact spans < 32 * 2^10 ids
+#endif
+#ifndef TCB_SMALL_FB2
+#define TCB_SMALL_FB2 1  // filter bits per id
+#endif
+static constexpr int kLwS = TCB_SMALL_LWS;
+static constexpr int kSmallFb = TCB_SMALL_FB2;
+static constexpr int kSmallCap = 128;  // 4 ids per lane
+static constexpr int kSmallSbW = kSbWords;
+
+// 16-byte streaming load: every chunk is read once per owner, so it should
+// not displace the L1 lines of the tables and descriptors.
+#ifndef TCB_LDMODE
+#define TCB_LDMODE 0
+#endif
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+#if TCB_LDMODE == 0
+  return __ldg(p);
+#else
+  int4 r;
+#if TCB_LDMODE == 1
+  asm("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#else
+  asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+#endif
+  return r;
+#endif
+}
+
+// Resolves chunk b + lane of the warp's flat chunk space (its segment, the
+// ids of the chunk inside that segment) and issues its load.  `fast`: the
+// group's start bitmap covers it (total <= 32 kSmallSbW); otherwise the
+// starts come from a ballot and a warp OR-reduction over the lanes' segment
+// starts.  Segment table entry: (chunk f of the segment is pool4[x + f],
+// (last chunk) << 8 | last-chunk id mask << 4 | first-chunk id mask).
+__device__ __forceinline__ void small_window(const int4* __restrict__ pool4, const int2* __restrict__ segtab,
+                                             const uint32_t* __restrict__ sbits, bool fast, bool lane_seg,
+                                             int excl, int total, int lane, int b, int& cbase, int4& v,
+                                             uint32_t& vm) {
+  const unsigned FULL = 0xffffffffu;
+  vm = 0;
+  v = make_int4(0, 0, 0, 0);
+  if (b >= total) return;  // warp-uniform
+  unsigned starts;
+  int sj;
+  if (fast) {
+    starts = sbits[b >> 5];
+    sj = cbase + __popc(starts & ((2u << lane) - 1u)) - 1;
+    cbase += __popc(starts);
+  } else {
+    const unsigned before = __ballot_sync(FULL, lane_seg && excl < b);
+    const unsigned bit = (lane_seg && excl >= b && excl < b + 32) ? (1u << (excl - b)) : 0u;
+    starts = __reduce_or_sync(FULL, bit);
+    sj = __popc(before) - 1 + __popc(starts & ((2u << lane) - 1u));
+  }
+  const int f = b + lane;
+  if (f < total) {
+    const int2 q = segtab[sj];
+    v = ld_stream(pool4 + (q.x + f));
+    uint32_t mk = 0xFu;
+    if ((starts >> lane) & 1u) mk &= (uint32_t)q.y & 0xFu;
+    if (f == (q.y >> 8)) mk &= ((uint32_t)q.y >> 4) & 0xFu;
+    vm = mk;
+  }
+}
+
+// Filter (kExactT false: two bits per id in one hashed word) or exact bitmap
+// (ids in [tlo, tlo + span)) test of the 4 ids of v; returns the hit mask.
+template <bool kExactT>
+__device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm, int32_t tlo, uint32_t span, int4 v,
+                                                uint32_t vm) {
+  const int32_t xs[4] = {v.x, v.y, v.z, v.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (kExactT) {
+      const uint32_t off = min((uint32_t)(xs[k] - tlo), span);
+      const uint32_t wd = bm[off >> 5];
+      m |= __funnelshift_r(wd, wd, off - k) & (1u << k);
+    } else {
+      const uint32_t h = tab_hash((uint32_t)xs[k]);
+      const uint32_t wd = bm[h >> (32 - kLwS)];
+      if (kSmallFb == 2)
+        m |= __funnelshift_r(wd, wd, h - k) & __funnelshift_r(wd, wd, (h >> 5) - k) & (1u << k);
+      else
+        m |= __funnelshift_r(wd, wd, h - k) & (1u << k);
+    }
+  }
+  return m & vm;
+}
+
+// Exact membership of the filter hits: the owner's list is held in
+// registers (lane l has ids l, l + 32, l + 64, l + 96; -1 pads), so each hit
+// (lane, id) is one shuffle, four compares and one ballot for the whole
+// warp.  Returns the number of true hits (warp-uniform).
+__device__ __forceinline__ uint32_t small_verify(uint32_t m, int4 v, int4 t, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  uint32_t c = 0;
+  unsigned any = __ballot_sync(FULL, m != 0);
+  while (any) {
+    const int src = __ffs(any) - 1;
+    const int k = __ffs(m) - 1;
+    int x = (k == 0) ? v.x : (k == 1) ? v.y : (k == 2) ? v.z : v.w;
+    x = __shfl_sync(FULL, x, src);
+    c += __ballot_sync(FULL, (t.x == x) | (t.y == x) | (t.z == x) | (t.w == x)) != 0u;
+    if (lane == src) m &= m - 1u;
+    any = __ballot_sync(FULL, m != 0);
+  }
+  return c;
+}
+
+template <bool kExactT>
+__device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int4 v,
+                                           uint32_t vm, int lane, uint32_t& cnt) {
+  const uint32_t m = small_probe<kExactT>(bm, tlo, span, v, vm);
+  if (kExactT) {
+    cnt += __popc(m);
+  } else {
+    const uint32_t c = small_verify(m, v, t, lane);
+    if (lane == 0) cnt += c;
+  }
+}
+
+// One warp streams segments [g0, g1) (<= 32) of the current owner.
+template <bool kExactT, class Segs>
+__device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __restrict__ pool,
+                                            const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int g0, int g1,
+                                            int lane, uint32_t& cnt, int2* segtab, uint32_t* sbits) {
+  const unsigned FULL = 0xffffffffu;
+  constexpr int kW = TCB_SMALL_W;
+  int s = 0, e = 0;
+  if (g0 + lane < g1) segs.get(g0 + lane, s, e);
+  const int len = e - s;
+  const unsigned nz = __ballot_sync(FULL, len > 0);  // compact non-empty segments to the low lanes
+  const int nseg = __popc(nz);
+  int src = lane;
+  if (nz & (nz + 1u)) src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
+  const int cs = __shfl_sync(FULL, s, src);
+  int clen = __shfl_sync(FULL, len, src);
+  if (lane >= nseg) clen = 0;
+  const int c0s = cs >> 2;
+  const int nch = (lane < nseg) ? ((cs + clen + 3) >> 2) - c0s : 0;
+  const int fm = (int)((0xFu << (cs & 3)) & 0xFu);
+  const int lm = (int)(0xFu >> (3 - ((cs + clen - 1) & 3)));
+  int incl = nch;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(FULL, incl, 31);
+  const int excl = incl - nch;
+  const bool fast = total <= 32 * kSmallSbW;
+  const bool lane_seg = lane < nseg;
+  __syncwarp();  // the previous group's reads of segtab / sbits are done
+  if (lane_seg) {
+    // chunk f of this segment is pool4[c0s - excl + f]; last chunk incl - 1 (< 2^23:
+    // oriented lists hold at most sqrt(2m) ids)
+    segtab[lane] = make_int2(c0s - excl, ((incl - 1) << 8) | (lm << 4) | fm);
+    if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
+  }
+  __syncwarp();
+  const int4* pool4 = reinterpret_cast<const int4*>(pool);
+  int cbase = 0;
+  int4 v[kW];
+  uint32_t vm[kW];
+#pragma unroll
+  for (int k = 0; k < kW; ++k)
+    small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, 32 * k, cbase, v[k], vm[k]);
+  for (int base = 0; base < total; base += 32 * kW) {
+#if TCB_SMALL_PIPE2
+    int4 nv[kW];
+    uint32_t nvm[kW];
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+      small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase, nv[k],
+                   nvm[k]);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) small_step<kExactT>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+      v[k] = nv[k];
+      vm[k] = nvm[k];
+    }
+#else
+#pragma unroll
+    for (int k = 0; k < kW; ++k) small_step<kExactT>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+    if (base + 32 * kW < total) {
+#pragma unroll
+      for (int k = 0; k < kW; ++k)
+        small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase, v[k],
+                     vm[k]);
+    }
+#endif
+  }
+  if (fast) {
+    __syncwarp();
+    if (lane_seg) sbits[excl >> 5] = 0;
+  }
+}
+
+template <class Segs>
+__global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a, Segs segs) {
+  __shared__ uint32_t filts[kWarps][1 << kLwS];
+  __shared__ int2 segtabs[kWarps][32];
+  __shared__ uint32_t sbitss[kWarps][kSmallSbW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* bm = filts[warp];
+  int2* segtab = segtabs[warp];
+  uint32_t* sbits = sbitss[warp];
+  const unsigned FULL = 0xffffffffu;
+  for (int i = lane; i < kSmallSbW; i += 32) sbits[i] = 0;
+  for (int i = lane; i < (1 << kLwS); i += 32) bm[i] = 0;
+  __syncwarp();
+  const int nch = *a.nchunks;
+  Acc acc;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(a.queue, 1) * a.stride + a.part;
+    c = __shfl_sync(FULL, c, 0);
+    if (c >= nch) break;
+    int r = (int)a.chunk_r[c];
+    const int r1 = (int)a.chunk_r[c + 1];
+    int x = a.chunk_x[c];
+    while (r < r1) {
+      x = advance_owner32(a, x, r, lane);
+      const int rb = min((int)__ldg(&a.row_indptr[x + 1]), r1);
+      const int ra = r;
+      r = rb;
+      const OwnerRef ow = resolve_owner(a, x);
+      const int so = (int)ow.seg_off;
+      const int d = ow.d;  // <= 128
+      acc.to_bucket(a, ow.u, lane);
+      const int32_t* gtab = a.tab_indices + ow.t0;
+      int4 t = make_int4(-1, -1, -1, -1);
+      t.x = lane < d ? __ldg(&gtab[lane]) : -1;
+      if (d > 32) t.y = lane + 32 < d ? __ldg(&gtab[lane + 32]) : -1;
+      if (d > 64) t.z = lane + 64 < d ? __ldg(&gtab[lane + 64]) : -1;
+      if (d > 96) t.w = lane + 96 < d ? __ldg(&gtab[lane + 96]) : -1;
+      const int32_t tlo = ow.tlo;
+      const uint32_t span = ow.span;
+      const int32_t tv[4] = {t.x, t.y, t.z, t.w};
+      if (span < (32u << kLwS)) {
+        // narrow id span: exact direct-mapped bitmap over [tlo, tlo + span)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tv[k] >= 0) {
+            const uint32_t off = (uint32_t)(tv[k] - tlo);
+            atomicOr(&bm[off >> 5], 1u << (off & 31));
+          }
+        __syncwarp();
+        for (int g = ra; g < rb; g += 32)
+          small_group<true>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt, segtab,
+                            sbits);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tv[k] >= 0) bm[(uint32_t)(tv[k] - tlo) >> 5] = 0;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tv[k] >= 0) filt_insert<kLwS, kSmallFb>(bm, tv[k]);
+        __syncwarp();
+        for (int g = ra; g < rb; g += 32)
+          small_group<false>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt, segtab,
+                             sbits);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (tv[k] >= 0) filt_clear<kLwS>(bm, tv[k]);
+      }
+      __syncwarp();
+    }
+    acc.fold();
+  }
+  acc.flush(a.out, lane);
+}
+
 // Block tier: owners with d > d_lo (the mid tier's cap).  The block stages the owner's table
 // once per chunk-owner and its 16 warps stream groups of 32 segments.
 template <class Segs>
@@ -1095,7 +1403,11 @@ static const TierShape& tier_shape() {
   static bool init = false;
   if (!init) {
     int per_sm = 0;
+#if TCB_SMALL_V20
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<PullSegs>, kThreads, 0));
+#else
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_SMALL(PullSegs), kThreads, 0));
+#endif
     ts.blocks[0] = std::max(per_sm, 1) * sm_count();
     ts.workers[0] = ts.blocks[0] * kWarps;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_MID(PullSegs), kMidWarps * 32, 0));
@@ -1367,7 +1679,11 @@ void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStre
     TC_CUDA(cudaEventRecord(g_tev[0], s));
   }
   if (L.hsz[0]) {
+#if TCB_SMALL_V20
+    k_small<Segs><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+#else
     K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+#endif
     check_launch();
   }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[1], s));
@@ -1420,8 +1736,10 @@ struct MiddlePlan {
   EngineLaunch L;
   int parts = 1;  // devices the chunk plan is cut for (tc_plan_middle_parts)
   cudaEvent_t ready = nullptr;  // recorded after the planning kernels; runs on any stream wait on it
+  cudaEvent_t done = nullptr;   // recorded behind each run: the next run (any stream) waits on it
   ~MiddlePlan() {
     if (ready) cudaEventDestroy(ready);
+    if (done) cudaEventDestroy(done);
   }
 };
 
@@ -1597,10 +1915,17 @@ int tc_plan_run_part(tc_plan_t plan, int32_t part, unsigned long long* out, tc_s
     if (P->u1 <= P->u0) return;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     TC_CUDA(cudaStreamIsCapturing(s, &cap));
-    if (cap == cudaStreamCaptureStatusNone) TC_CUDA(cudaStreamWaitEvent(s, P->ready, 0));
+    if (cap == cudaStreamCaptureStatusNone) {
+      TC_CUDA(cudaStreamWaitEvent(s, P->ready, 0));
+      // the plan's queue counters are shared: a run on another stream must
+      // not reset them while an earlier run still claims chunks
+      if (!P->done) TC_CUDA(cudaEventCreateWithFlags(&P->done, cudaEventDisableTiming));
+      else TC_CUDA(cudaStreamWaitEvent(s, P->done, 0));
+    }
     const tcb::PullSegs segs{reinterpret_cast<const int2*>(P->rev_seg)};
     if (part < 0) tcb::launch_engine(P->L, out, segs, s);  // every chunk
     else tcb::launch_engine(P->L, out, segs, s, part, P->parts);
+    if (cap == cudaStreamCaptureStatusNone) TC_CUDA(cudaEventRecord(P->done, s));
   });
 }
 

@@ -32,8 +32,14 @@ def _as_device_pairs(edges, dev):
     if isinstance(edges, torch.Tensor):
         t = edges.reshape(-1, 2)
         if t.dtype != torch.int32:
-            if t.numel() and int(t.max()) > _I32_MAX:
-                raise ValueError("node labels must fit int32 on the B200 path")
+            if t.numel():
+                lo, hi = torch.aminmax(t)
+                # checked before the cast: an int64 label below -2^31 would wrap
+                # to a non-negative int32 id (graph.py:87-88 rejects negatives)
+                if int(lo) < 0:
+                    raise ValueError("negative node id in edge list")
+                if int(hi) > _I32_MAX:
+                    raise ValueError("node labels must fit int32 on the B200 path")
             t = t.to(torch.int32)
         return t.to(dev, non_blocking=True).contiguous()
     a = np.asarray(edges)

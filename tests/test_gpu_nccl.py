@@ -70,5 +70,6 @@ def test_bench_multi_gpu_path_world1(mode, tmp_path):
     out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
-    assert line["config"]["triangles"] == 722 and line["n_gpus"] == 1
-    assert {"replicated": "replicated", "surrogate": "surrogate", "direct": "pull"}[mode] in line["config"]["parallelism"]
+    assert line["workload_detail"]["triangles"] == 722 and line["n_gpus"] == 1
+    assert {"replicated": "replicated", "surrogate": "surrogate", "direct": "pull"}[mode] in \
+        line["workload_detail"]["parallelism"]

@@ -11,4 +11,4 @@ for f in csrc/*.cu; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/lib_$name.so $tmp/*.o -lcudart_static -lrt -lpthread -ldl
-echo "$name: $(grep -A3 'k_engineINS_8PullSegs' $tmp/count.log | grep -E 'Used|spill' | tr -s ' ' | tr '\n' ' ')"
+echo "$name: $(grep -E -A3 'k_(engine|small)INS_8PullSegs' $tmp/count.log | grep -E 'Used|spill' | tr -s ' ' | tr '\n' ' ')"

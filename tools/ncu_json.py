@@ -1,4 +1,4 @@
-"""DRAM bytes per engine launch from an ncu report -> profiles/ncu_engine_<cfg>.json (dev tool)."""
+"""DRAM bytes per engine launch (stamped with the sha of csrc/count.cu it was captured from) from an ncu report -> profiles/ncu_engine_<cfg>.json (dev tool)."""
 import csv
 import io
 import json
@@ -19,6 +19,10 @@ for r in rows[2:]:
     ks.append({"kernel": r[hdr.index("Kernel Name")],
                "duration_ms": val("gpu__time_duration.sum", tscale),
                "dram_bytes": val("dram__bytes_read.sum", scale) + val("dram__bytes_write.sum", scale)})
-json.dump({"source": src, "kernels": ks, "dram_bytes_per_launch": sum(k["dram_bytes"] for k in ks)},
+import hashlib
+import os
+cu = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1406_5687_b200", "csrc", "count.cu")
+sha = hashlib.sha256(open(cu, "rb").read()).hexdigest()[:16]
+json.dump({"source": src, "count_cu_sha": sha, "kernels": ks, "dram_bytes_per_launch": sum(k["dram_bytes"] for k in ks)},
           open(out, "w"), indent=1)
 print(json.dumps(ks, indent=1))
