@@ -85,14 +85,23 @@ int tc_normalize_host(const int32_t* host_edges, int64_t m_raw, int32_t* dev_edg
  *   relabel, orig_ids, deg, eff_deg  int32[n]
  *   rev_indptr int64[n+1]   predecessor rows: one entry per v with u in N^_v,
  *                           in unspecified order (the engine sums over a row)
- *   rev_seg    int32[2*m]   (e+1, eff_indptr[v+1]) of the edge e = (v, u): the
- *                           suffix of N^_v after u (m < 2^31 so int32 fits)
+ *   rev_seg    int32[2*m]   the suffix of N^_v after u of the edge e = (v, u),
+ *                           as [start, end) in pool coordinates
  *   rev_cost   int64[n+1]   exclusive prefix over u of the pull-engine cost
+ *   pool_indptr int64[n+1]  row offsets of the padded pool (multiples of 4)
+ *   pool       int32[TC_POOL_HEAD + m + 3n + 4] buffer; pass the pointer
+ *                           TC_POOL_HEAD ids past its start: pool[-TC_POOL_HEAD..-1]
+ *                           = INT32_MAX, row v = N^_v at pool[pool_indptr[v]..]
+ *                           padded with INT32_MAX to a multiple of 4 ids, so a
+ *                           16-byte chunk never mixes two rows (the engine's
+ *                           mask-free streaming, tc_count_middle pool_padded)
  * Asynchronous. */
+#define TC_POOL_HEAD 512
 int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                    int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                    int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                   int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
+                   int32_t* rev_seg, int64_t* rev_cost, int64_t* pool_indptr, int32_t* pool,
+                   tc_stream_t stream);
 
 /* tc_build_graph in degree order with the degree array given (deg_hint
  * int32[n], e.g. from tc_normalize_host with *deg_valid): skips the degree
@@ -101,13 +110,15 @@ int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* or
 int tc_build_graph_deg(const int32_t* edges, int64_t m, int64_t n, const int32_t* deg_hint,
                        int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                        int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                       int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream);
+                       int32_t* rev_seg, int64_t* rev_cost, int64_t* pool_indptr, int32_t* pool,
+                       tc_stream_t stream);
 
 /* Full CSR (graph.py:125-127) assembled from the forward and reverse CSRs:
- * row u = its neighbours ascending (predecessors, then N^_u).  full_indptr
- * int64[n+1], full_indices int32[2m].  Synchronises. */
+ * row u = its neighbours ascending (predecessors, then N^_u).  pool_indptr:
+ * the row offsets rev_seg's coordinates refer to (tc_build_graph's).
+ * full_indptr int64[n+1], full_indices int32[2m].  Synchronises. */
 int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
-                  const int64_t* rev_indptr, const int32_t* rev_seg, int64_t n,
+                  const int64_t* rev_indptr, const int32_t* rev_seg, const int64_t* pool_indptr, int64_t n,
                   int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream);
 
 /* ---------------------------------------------------------------- count */
@@ -117,13 +128,17 @@ int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
  * (int64[nbuckets+1], ascending) bins u; NULL with nbuckets==1 sums all.
  * Table lists N^_u come from (tab_indptr, tab_indices) indexed by u;
  * predecessor suffixes are rev_seg int32 pairs indexing `pool` (int32).
- * On one GPU pool == eff_indices.  out is overwritten (not accumulated).
+ * pool_padded = 1: `pool` is tc_build_graph's row-padded pool (rows at
+ * multiples of 4 ids, INT32_MAX padding and TC_POOL_HEAD INT32_MAX ids before
+ * pool[0]) and the engine streams it without per-chunk id masks; 0: any
+ * 16-byte aligned pool padded by >= 4 ids at its end (e.g. received lists).
+ * out is overwritten (not accumulated).
  * This is count_node_range(0, n) (_kernels.py:40-52) for the whole range,
  * and the per-rank partials of count_space_surrogate for rank buckets. */
 int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
                     const int64_t* rev_indptr, const int32_t* rev_seg,
-                    const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
-                    int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                    const int64_t* rev_cost, const int32_t* pool, int32_t pool_padded, int64_t n,
+                    int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, tc_stream_t stream);
 
 /* Reusable form of tc_count_middle for repeated counts of one graph: the
@@ -139,9 +154,9 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
  * the previous run recorded behind its engine launches. */
 typedef struct tc_plan_s* tc_plan_t;
 int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
-                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
-                   tc_stream_t stream);
+                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int32_t pool_padded,
+                   int64_t n, int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                   tc_plan_t* plan, tc_stream_t stream);
 int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream);
 int tc_plan_free(tc_plan_t plan);
 
@@ -153,9 +168,9 @@ int tc_plan_free(tc_plan_t plan);
  * tc_plan_run).  Every tier is split, so the parts stay balanced whatever
  * the cost model's error between tiers; the part counts sum to the total. */
 int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                         const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n,
-                         int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, int32_t nparts,
-                         tc_plan_t* plan, tc_stream_t stream);
+                         const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int32_t pool_padded,
+                         int64_t n, int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                         int32_t nparts, tc_plan_t* plan, tc_stream_t stream);
 int tc_plan_run_part(tc_plan_t plan, int32_t part, unsigned long long* out, tc_stream_t stream);
 
 /* Generic engine over k "virtual owners": owner x probes the table list
@@ -175,9 +190,10 @@ int tc_count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const
  * (tile(v), u, v); each (tile, u) with entries is one virtual owner.
  * Outputs (capacity E = rev_indptr[u1] - rev_indptr[u0]): owner_u int32[E],
  * owner_ptr int64[E+1], segs int32[2E], cost_prefix int64[E+1]; returns the
- * owner count k and the tile count.  Feed to tc_count_owners (mode 1).
+ * owner count k and the tile count.  pool_indptr: the row offsets rev_seg's
+ * coordinates refer to.  Feed to tc_count_owners (mode 1).
  * Synchronises. */
-int tc_tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
+int tc_tile_pull(const int64_t* eff_indptr, const int64_t* pool_indptr, int64_t n, const int64_t* rev_indptr,
                  const int32_t* rev_seg, int64_t u0, int64_t u1,
                  int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int32_t* segs,
                  int64_t* cost_prefix, int64_t* k_host, int64_t* ntiles_host, tc_stream_t stream);

@@ -26,20 +26,20 @@ _SIGS = {
     "tc_abi_version": [],
     "tc_trim_pool": [],
     "tc_normalize": [_vp, _i64, _vp, _pi64, _pi64, _vp],
-    "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "tc_build_graph_deg": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "tc_build_graph_deg": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "tc_normalize_host": [_vp, _i64, _vp, _vp, _pi64, _pi64, _vp, _vp, _vp],
-    "tc_build_full": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
-    "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
+    "tc_build_full": [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
-    "tc_plan_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_vp), _vp],
+    "tc_plan_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_vp), _vp],
     "tc_plan_run": [_vp, _vp, _vp],
-    "tc_plan_middle_parts": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i32, _i32, ctypes.POINTER(_vp),
-                             _vp],
+    "tc_plan_middle_parts": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, _i32,
+                             ctypes.POINTER(_vp), _vp],
     "tc_plan_run_part": [_vp, _i32, _vp, _vp],
     "tc_plan_free": [_vp],
     "tc_count_owners": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32, _vp, _i32, _vp],
-    "tc_tile_pull": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
+    "tc_tile_pull": [_vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "tc_intersect_count": [_vp, _i64, _vp, _i64, _vp, _vp],
     "tc_engine_timing": [_i32, _vp, _vp, _vp],
     "tc_set_tuning": [_i32, _i64],

@@ -315,7 +315,7 @@ static constexpr int kRevSpan = 1024;
 __global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
                               int64_t n, int64_t m, const int64_t* __restrict__ rev_indptr,
                               const int64_t* __restrict__ bounds, int ph, int32_t* cursor, int32_t* back,
-                              int2* rev_seg) {
+                              int2* rev_seg, const int64_t* __restrict__ pool_indptr, int32_t* pool) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -323,21 +323,42 @@ __global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int3
   for (int64_t e0 = warp * kRevSpan; e0 < m; e0 += nwarps * kRevSpan) {
     const int64_t e1 = min(m, e0 + kRevSpan);
     int64_t v = row_of_edge(eff_indptr, n, e0);
-    int64_t vend = eff_indptr[v + 1];
+    int64_t vbeg = eff_indptr[v], vend = eff_indptr[v + 1];
     for (int64_t c = e0; c < e1; c += 32) {
       const int64_t e = min(c + lane, e1 - 1);
-      int64_t w = v, wend = vend;
-      while (wend <= e) wend = eff_indptr[++w + 1];
+      int64_t w = v, wbeg = vbeg, wend = vend;
+      while (wend <= e) {
+        wbeg = wend;
+        wend = eff_indptr[++w + 1];
+      }
       v = __shfl_sync(0xffffffffu, w, 31);
+      vbeg = __shfl_sync(0xffffffffu, wbeg, 31);
       vend = __shfl_sync(0xffffffffu, wend, 31);
       if (c + lane >= e1) continue;
       const int64_t u = eff_indices[e];
+      const int64_t p0 = pool_indptr[w];  // row w of the padded pool
+      if (ph == 0) {  // the padded pool: row w's ids, then INT32_MAX up to a multiple of 4
+        pool[p0 + (e - wbeg)] = (int32_t)u;
+        if (e + 1 == wend)
+          for (int64_t q = p0 + (wend - wbeg); q < pool_indptr[w + 1]; ++q) pool[q] = INT32_MAX;
+      }
       if (u < u0 || u >= u1) continue;
       const int64_t slot = (e + 1 < wend) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
                                           : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
-      rev_seg[slot] = make_int2((int)(e + 1), (int)wend);
+      // the suffix of N^_w after u, in pool coordinates
+      rev_seg[slot] = make_int2((int)(p0 + (e + 1 - wbeg)), (int)(p0 + (wend - wbeg)));
     }
   }
+}
+
+// Padded pool row sizes (multiples of 4 ids: a 16-byte chunk never holds
+// ids of two rows) and the INT32_MAX head before the pool.
+__global__ void k_pool_sizes(const int64_t* __restrict__ eff_indptr, int64_t n, int64_t* sz) {
+  GRID_STRIDE(v, n + 1) sz[v] = (v < n) ? ((eff_indptr[v + 1] - eff_indptr[v] + 3) & ~(int64_t)3) : 0;
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t k, int32_t val) {
+  GRID_STRIDE(i, k) p[i] = val;
 }
 
 // Row sorts after the counting scatter.  CUB's segmented sort handles rows
@@ -495,7 +516,8 @@ __global__ void k_rev_cost_fin(const int64_t* __restrict__ rev_indptr, const int
 // rows are sorted afterwards.
 __global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __restrict__ eff_indices,
                        const int64_t* __restrict__ rev_indptr, const int2* __restrict__ rev_seg,
-                       int64_t n, int64_t* full_indptr, int32_t* full_indices) {
+                       const int64_t* __restrict__ pool_indptr, int64_t n, int64_t* full_indptr,
+                       int32_t* full_indices) {
   int lane = threadIdx.x & 31;
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -505,7 +527,7 @@ __global__ void k_full(const int64_t* __restrict__ eff_indptr, const int32_t* __
     if (u == n) continue;
     int64_t r0 = rev_indptr[u], r1 = rev_indptr[u + 1];
     for (int64_t r = r0 + lane; r < r1; r += 32)
-      full_indices[base + (r - r0)] = (int32_t)row_of_edge(eff_indptr, n, (int64_t)rev_seg[r].x - 1);
+      full_indices[base + (r - r0)] = (int32_t)row_of_edge(pool_indptr, n, (int64_t)rev_seg[r].x - 1);
     int64_t e0 = eff_indptr[u], e1 = eff_indptr[u + 1];
     int64_t off = base + (r1 - r0);
     for (int64_t e = e0 + lane; e < e1; e += 32) full_indices[off + (e - e0)] = eff_indices[e];
@@ -943,7 +965,8 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
 void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                  int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel, int32_t* orig_ids,
                  int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr, int32_t* rev_seg,
-                 int64_t* rev_cost, cudaStream_t s, const int32_t* deg_hint = nullptr) {
+                 int64_t* rev_cost, int64_t* pool_indptr, int32_t* pool, cudaStream_t s,
+                 const int32_t* deg_hint = nullptr) {
   TC_REQUIRE(n >= 0 && m >= 0, TC_EINVAL, "negative size");
   TC_REQUIRE(n < (1ll << 31) - 1, TC_EINVAL, "n must fit int32 ids");
   TC_REQUIRE(m < (1ll << 31) - 1, TC_EINVAL, "m must be < 2^31");
@@ -968,10 +991,14 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     }
     deg_orig = h;
   }
+  // the pool's INT32_MAX head (TC_POOL_HEAD ids before pool[0])
+  k_fill_i32<<<1, 256, 0, s>>>(pool - TC_POOL_HEAD, TC_POOL_HEAD, INT32_MAX);
+  check_launch();
   if (n == 0) {
     TC_CUDA(cudaMemsetAsync(eff_indptr, 0, sizeof(int64_t), s));
     TC_CUDA(cudaMemsetAsync(rev_indptr, 0, sizeof(int64_t), s));
     TC_CUDA(cudaMemsetAsync(rev_cost, 0, sizeof(int64_t), s));
+    TC_CUDA(cudaMemsetAsync(pool_indptr, 0, sizeof(int64_t), s));
     return;
   }
   // canonical order: ascending (degree, id) via a stable radix sort (graph.py:152)
@@ -1062,6 +1089,16 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     void* t = sc.bytes(tmp);
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in_deg, rev_indptr, n + 1, s));
   }
+  // padded pool row offsets (rows filled by the reverse scatter's first phase)
+  {
+    int64_t* psz = sc.alloc<int64_t>(n + 1);
+    k_pool_sizes<<<grid_for(n + 1, kBlock), kBlock, 0, s>>>(eff_indptr, n, psz);
+    check_launch();
+    size_t tmp = 0;
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, psz, pool_indptr, n + 1, s));
+    void* t = sc.bytes(tmp);
+    TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, psz, pool_indptr, n + 1, s));
+  }
   if (m) {
     int32_t* cursor = sc.alloc<int32_t>(2 * n);
     TC_CUDA(cudaMemsetAsync(cursor, 0, 2 * n * sizeof(int32_t), s));
@@ -1070,7 +1107,8 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     check_launch();
     for (int ph = 0; ph < nph; ++ph) {
       k_rev_scatter<<<grid_for((m + kRevSpan - 1) / kRevSpan * 32, kBlock, sms * 16), kBlock, 0, s>>>(
-          eff_indptr, eff_indices, n, m, rev_indptr, bounds, ph, cursor, cursor + n, reinterpret_cast<int2*>(rev_seg));
+          eff_indptr, eff_indices, n, m, rev_indptr, bounds, ph, cursor, cursor + n, reinterpret_cast<int2*>(rev_seg),
+          pool_indptr, pool);
       check_launch();
     }
   }
@@ -1168,21 +1206,23 @@ int tc_normalize(const int32_t* edges, int64_t m_raw, int32_t* out_edges, int64_
 int tc_build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
                    int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                    int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                   int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
+                   int32_t* rev_seg, int64_t* rev_cost, int64_t* pool_indptr, int32_t* pool,
+                   tc_stream_t stream) {
   return tcb::guarded([&] {
     tcb::build_graph(edges, m, n, order, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
-                     rev_indptr, rev_seg, rev_cost, (cudaStream_t)stream);
+                     rev_indptr, rev_seg, rev_cost, pool_indptr, pool, (cudaStream_t)stream);
   });
 }
 
 int tc_build_graph_deg(const int32_t* edges, int64_t m, int64_t n, const int32_t* deg_hint,
                        int64_t* eff_indptr, int32_t* eff_indices, int32_t* relabel,
                        int32_t* orig_ids, int32_t* deg, int32_t* eff_deg, int64_t* rev_indptr,
-                       int32_t* rev_seg, int64_t* rev_cost, tc_stream_t stream) {
+                       int32_t* rev_seg, int64_t* rev_cost, int64_t* pool_indptr, int32_t* pool,
+                       tc_stream_t stream) {
   return tcb::guarded([&] {
     TC_REQUIRE(deg_hint != nullptr, TC_EINVAL, "NULL deg_hint");
     tcb::build_graph(edges, m, n, nullptr, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg,
-                     rev_indptr, rev_seg, rev_cost, (cudaStream_t)stream, deg_hint);
+                     rev_indptr, rev_seg, rev_cost, pool_indptr, pool, (cudaStream_t)stream, deg_hint);
   });
 }
 
@@ -1195,7 +1235,7 @@ int tc_normalize_host(const int32_t* host_edges, int64_t m_raw, int32_t* dev_edg
 }
 
 int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
-                  const int64_t* rev_indptr, const int32_t* rev_seg, int64_t n,
+                  const int64_t* rev_indptr, const int32_t* rev_seg, const int64_t* pool_indptr, int64_t n,
                   int64_t* full_indptr, int32_t* full_indices, tc_stream_t stream) {
   return tcb::guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
@@ -1211,7 +1251,8 @@ int tc_build_full(const int64_t* eff_indptr, const int32_t* eff_indices,
     tcb::Scratch sc(s);
     int32_t* unsorted = sc.alloc<int32_t>(m2 > 0 ? m2 : 1);
     tcb::k_full<<<tcb::grid_for((n + 1) * 32, 256, sms * 16), 256, 0, s>>>(
-        eff_indptr, eff_indices, rev_indptr, reinterpret_cast<const int2*>(rev_seg), n, full_indptr, unsorted);
+        eff_indptr, eff_indices, rev_indptr, reinterpret_cast<const int2*>(rev_seg), pool_indptr, n, full_indptr,
+        unsorted);
     tcb::check_launch();
     if (m2 > 0) {  // predecessor rows are unordered (k_rev_scatter): sort every row
       TC_REQUIRE(m2 < (1ll << 31), TC_EINVAL, "full CSR too large");

@@ -631,6 +631,10 @@ struct EngineArgs {
   // between them (replicated multi-GPU count); 1 / 0 runs them all.
   int stride = 1;
   int part = 0;
+  // The pool is row-padded (tc_build_graph's padded pool: every row starts
+  // at a multiple of 4 ids, is padded with INT32_MAX, and TC_POOL_HEAD
+  // INT32_MAX ids precede pool[0]): the small tier streams without id masks.
+  int padded = 0;
 };
 
 struct OwnerRef {
@@ -902,6 +906,7 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
 // starts come from a ballot and a warp OR-reduction over the lanes' segment
 // starts.  Segment table entry: (chunk f of the segment is pool4[x + f],
 // (last chunk) << 8 | last-chunk id mask << 4 | first-chunk id mask).
+template <bool kPadded>
 __device__ __forceinline__ void small_window(const int4* __restrict__ pool4, const int2* __restrict__ segtab,
                                              const uint32_t* __restrict__ sbits, bool fast, bool lane_seg,
                                              int excl, int total, int lane, int b, int& cbase, int4& v,
@@ -920,10 +925,17 @@ __device__ __forceinline__ void small_window(const int4* __restrict__ pool4, con
     const unsigned before = __ballot_sync(FULL, lane_seg && excl < b);
     const unsigned bit = (lane_seg && excl >= b && excl < b + 32) ? (1u << (excl - b)) : 0u;
     starts = __reduce_or_sync(FULL, bit);
+    if (kPadded && (unsigned)(total - b) < 32u) starts |= 1u << (total - b);  // the tail segment
     sj = __popc(before) - 1 + __popc(starts & ((2u << lane) - 1u));
   }
   const int f = b + lane;
-  if (f < total) {
+  if (kPadded) {
+    // chunks past `total` resolve to the tail segment (INT32_MAX head of the
+    // pool); ids before a suffix's start in its first chunk are <= u and ids
+    // after a row's end are INT32_MAX padding: neither is in N^_u, so no mask
+    v = __ldg(pool4 + (reinterpret_cast<const int*>(segtab)[2 * sj] + f));
+    vm = 0xFu;
+  } else if (f < total) {
     const int2 q = segtab[sj];
     v = ld_stream(pool4 + (q.x + f));
     uint32_t mk = 0xFu;
@@ -935,7 +947,7 @@ __device__ __forceinline__ void small_window(const int4* __restrict__ pool4, con
 
 // Filter (kExactT false: two bits per id in one hashed word) or exact bitmap
 // (ids in [tlo, tlo + span)) test of the 4 ids of v; returns the hit mask.
-template <bool kExactT>
+template <bool kExactT, bool kPadded>
 __device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm, int32_t tlo, uint32_t span, int4 v,
                                                 uint32_t vm) {
   const int32_t xs[4] = {v.x, v.y, v.z, v.w};
@@ -955,7 +967,7 @@ __device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm,
         m |= __funnelshift_r(wd, wd, h - k) & (1u << k);
     }
   }
-  return m & vm;
+  return kPadded ? m : (m & vm);
 }
 
 // Exact membership of the filter hits: the owner's list is held in
@@ -978,10 +990,10 @@ __device__ __forceinline__ uint32_t small_verify(uint32_t m, int4 v, int4 t, int
   return c;
 }
 
-template <bool kExactT>
+template <bool kExactT, bool kPadded>
 __device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int4 v,
                                            uint32_t vm, int lane, uint32_t& cnt) {
-  const uint32_t m = small_probe<kExactT>(bm, tlo, span, v, vm);
+  const uint32_t m = small_probe<kExactT, kPadded>(bm, tlo, span, v, vm);
   if (kExactT) {
     cnt += __popc(m);
   } else {
@@ -991,7 +1003,10 @@ __device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint
 }
 
 // One warp streams segments [g0, g1) (<= 32) of the current owner.
-template <bool kExactT, class Segs>
+// kPadded: a tail segment (index nseg, starting at chunk `total`) maps the
+// chunks past the group's end onto the pool's INT32_MAX head, so window
+// lanes need no bounds check.
+template <bool kExactT, bool kPadded, class Segs>
 __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __restrict__ pool,
                                             const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int g0, int g1,
                                             int lane, uint32_t& cnt, int2* segtab, uint32_t* sbits) {
@@ -1019,7 +1034,7 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
   }
   const int total = __shfl_sync(FULL, incl, 31);
   const int excl = incl - nch;
-  const bool fast = total <= 32 * kSmallSbW;
+  const bool fast = kPadded ? total < 32 * kSmallSbW : total <= 32 * kSmallSbW;
   const bool lane_seg = lane < nseg;
   __syncwarp();  // the previous group's reads of segtab / sbits are done
   if (lane_seg) {
@@ -1028,6 +1043,11 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
     segtab[lane] = make_int2(c0s - excl, ((incl - 1) << 8) | (lm << 4) | fm);
     if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
   }
+  if (kPadded && lane == 0) {
+    // tail segment: chunk f >= total reads pool4[f - total - 32], in the head
+    segtab[nseg] = make_int2(-total - 32, 0);
+    if (fast) atomicOr(&sbits[total >> 5], 1u << (total & 31));
+  }
   __syncwarp();
   const int4* pool4 = reinterpret_cast<const int4*>(pool);
   int cbase = 0;
@@ -1035,17 +1055,17 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
   uint32_t vm[kW];
 #pragma unroll
   for (int k = 0; k < kW; ++k)
-    small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, 32 * k, cbase, v[k], vm[k]);
+    small_window<kPadded>(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, 32 * k, cbase, v[k], vm[k]);
   for (int base = 0; base < total; base += 32 * kW) {
 #if TCB_SMALL_PIPE2
     int4 nv[kW];
     uint32_t nvm[kW];
 #pragma unroll
     for (int k = 0; k < kW; ++k)
-      small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase, nv[k],
-                   nvm[k]);
+      small_window<kPadded>(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase,
+                            nv[k], nvm[k]);
 #pragma unroll
-    for (int k = 0; k < kW; ++k) small_step<kExactT>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
 #pragma unroll
     for (int k = 0; k < kW; ++k) {
       v[k] = nv[k];
@@ -1053,25 +1073,26 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
     }
 #else
 #pragma unroll
-    for (int k = 0; k < kW; ++k) small_step<kExactT>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
     if (base + 32 * kW < total) {
 #pragma unroll
       for (int k = 0; k < kW; ++k)
-        small_window(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase, v[k],
-                     vm[k]);
+        small_window<kPadded>(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase,
+                              v[k], vm[k]);
     }
 #endif
   }
   if (fast) {
     __syncwarp();
     if (lane_seg) sbits[excl >> 5] = 0;
+    if (kPadded && lane == 0) sbits[total >> 5] = 0;
   }
 }
 
-template <class Segs>
+template <class Segs, bool kPadded>
 __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a, Segs segs) {
   __shared__ uint32_t filts[kWarps][1 << kLwS];
-  __shared__ int2 segtabs[kWarps][32];
+  __shared__ int2 segtabs[kWarps][33];
   __shared__ uint32_t sbitss[kWarps][kSmallSbW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* bm = filts[warp];
@@ -1119,8 +1140,8 @@ __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a
           }
         __syncwarp();
         for (int g = ra; g < rb; g += 32)
-          small_group<true>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt, segtab,
-                            sbits);
+          small_group<true, kPadded>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt,
+                                     segtab, sbits);
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -1131,8 +1152,8 @@ __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a
           if (tv[k] >= 0) filt_insert<kLwS, kSmallFb>(bm, tv[k]);
         __syncwarp();
         for (int g = ra; g < rb; g += 32)
-          small_group<false>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt, segtab,
-                             sbits);
+          small_group<false, kPadded>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt,
+                                      segtab, sbits);
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -1404,7 +1425,7 @@ static const TierShape& tier_shape() {
   if (!init) {
     int per_sm = 0;
 #if TCB_SMALL_V20
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<PullSegs>, kThreads, 0));
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_small<PullSegs, true>, kThreads, 0));
 #else
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_SMALL(PullSegs), kThreads, 0));
 #endif
@@ -1582,7 +1603,7 @@ template <class Segs, class Alloc>
 EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const int64_t* row_indptr,
                             const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* pool, int64_t x0,
                             int64_t x1, const int64_t* bucket_bounds, int nbuckets, Segs segs, cudaStream_t s,
-                            const int32_t* owner_map = nullptr, int mode = 0, int parts = 1) {
+                            const int32_t* owner_map = nullptr, int mode = 0, int parts = 1, int padded = 0) {
   const TierShape& ts = tier_shape();
   const int64_t nx = x1 - x0;
   const int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
@@ -1651,6 +1672,7 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
     L.args[k] = EngineArgs{vrow, tab_indptr, tab_indices, pool, chunk_r, chunk_x, ctl, ctl + 1,
                            bucket_bounds, nbuckets, nullptr, nx, owner_map, lo, hi, g_big_cap, own, row_indptr,
                            desc_a, desc_b};
+    L.args[k].padded = padded;
     L.queue[k] = ctl + 1;
   }
   return L;
@@ -1680,7 +1702,8 @@ void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStre
   }
   if (L.hsz[0]) {
 #if TCB_SMALL_V20
-    k_small<Segs><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    if (L.args[0].padded) k_small<Segs, true><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    else k_small<Segs, false><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
 #else
     K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
 #endif
@@ -1715,10 +1738,10 @@ template <class Segs>
 void run_engine(Scratch& sc, int64_t n_owner, const int64_t* cp, const int64_t* row_indptr, const int64_t* tab_indptr,
                 const int32_t* tab_indices, const int32_t* pool, int64_t x0, int64_t x1,
                 const int64_t* bucket_bounds, int nbuckets, unsigned long long* out, Segs segs,
-                cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0) {
+                cudaStream_t s, const int32_t* owner_map = nullptr, int mode = 0, int padded = 0) {
   (void)n_owner;
   EngineLaunch L = prepare_engine(sc, sc, cp, row_indptr, tab_indptr, tab_indices, pool, x0, x1, bucket_bounds,
-                                  nbuckets, segs, s, owner_map, mode);
+                                  nbuckets, segs, s, owner_map, mode, 1, padded);
   launch_engine(L, out, segs, s);
 }
 
@@ -1735,6 +1758,7 @@ struct MiddlePlan {
   Persist mem;
   EngineLaunch L;
   int parts = 1;  // devices the chunk plan is cut for (tc_plan_middle_parts)
+  int padded = 0;  // pool is tc_build_graph's row-padded pool
   cudaEvent_t ready = nullptr;  // recorded after the planning kernels; runs on any stream wait on it
   cudaEvent_t done = nullptr;   // recorded behind each run: the next run (any stream) waits on it
   ~MiddlePlan() {
@@ -1754,7 +1778,7 @@ static void plan_build(MiddlePlan& P, cudaStream_t s) {
   Scratch sc(s);
   P.L = prepare_engine(P.mem, sc, P.rev_cost, P.rev_indptr, P.tab_indptr, P.tab_indices, P.pool, P.u0, P.u1,
                        P.bucket_bounds, P.nbuckets, PullSegs{reinterpret_cast<const int2*>(P.rev_seg)}, s,
-                       nullptr, 1, P.parts);
+                       nullptr, 1, P.parts, P.padded);
   // no host synchronisation: a run waits on this event (pool memory of the
   // plan becomes valid on the run's stream through it)
   if (!P.ready) TC_CUDA(cudaEventCreateWithFlags(&P.ready, cudaEventDisableTiming));
@@ -1762,7 +1786,7 @@ static void plan_build(MiddlePlan& P, cudaStream_t s) {
 }
 
 void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                  const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n,
+                  const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int pool_padded, int64_t n,
                   int64_t u0, int64_t u1, const int64_t* bucket_bounds, int nbuckets,
                   unsigned long long* out, cudaStream_t s) {
   TC_REQUIRE(0 <= u0 && u0 <= u1 && u1 <= n, TC_EINVAL, "bad owner range");
@@ -1773,7 +1797,7 @@ void count_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const i
   if (u1 <= u0) return;
   Scratch sc(s);
   run_engine(sc, n, rev_cost, rev_indptr, tab_indptr, tab_indices, pool, u0, u1, bucket_bounds,
-             nbuckets, out, PullSegs{reinterpret_cast<const int2*>(rev_seg)}, s, nullptr, 1);
+             nbuckets, out, PullSegs{reinterpret_cast<const int2*>(rev_seg)}, s, nullptr, 1, pool_padded);
 }
 
 void count_owners(const int64_t* tab_indptr, const int32_t* tab_indices, const int32_t* owner_map,
@@ -1862,19 +1886,19 @@ extern "C" {
 
 int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
                     const int64_t* rev_indptr, const int32_t* rev_seg, const int64_t* rev_cost,
-                    const int32_t* pool, int64_t n, int64_t u0, int64_t u1,
+                    const int32_t* pool, int32_t pool_padded, int64_t n, int64_t u0, int64_t u1,
                     const int64_t* bucket_bounds, int32_t nbuckets, unsigned long long* out,
                     tc_stream_t stream) {
   return tcb::guarded([&] {
-    tcb::count_middle(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, n, u0, u1,
+    tcb::count_middle(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, pool_padded, n, u0, u1,
                       bucket_bounds, nbuckets, out, (cudaStream_t)stream);
   });
 }
 
 int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
-                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, int32_t nparts,
-                         tc_plan_t* plan, tc_stream_t stream) {
+                         const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int32_t pool_padded,
+                         int64_t n, int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                         int32_t nparts, tc_plan_t* plan, tc_stream_t stream) {
   return tcb::guarded([&] {
     TC_REQUIRE(plan != nullptr, TC_EINVAL, "plan out-pointer is NULL");
     *plan = nullptr;
@@ -1884,7 +1908,7 @@ int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, 
     TC_REQUIRE(bucket_bounds || nbuckets == 1, TC_EINVAL, "bucket_bounds required for nbuckets > 1");
     TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned");
     auto* P = new tcb::MiddlePlan{tab_indptr, rev_indptr, rev_cost, bucket_bounds, tab_indices, rev_seg, pool,
-                                  n, u0, u1, nbuckets, {0, 0, 0}, {}, {}, nparts};
+                                  n, u0, u1, nbuckets, {0, 0, 0}, {}, {}, nparts, pool_padded != 0};
     try {
       tcb::plan_build(*P, (cudaStream_t)stream);
     } catch (...) {
@@ -1896,10 +1920,10 @@ int tc_plan_middle_parts(const int64_t* tab_indptr, const int32_t* tab_indices, 
 }
 
 int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const int64_t* rev_indptr,
-                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int64_t n, int64_t u0,
-                   int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets, tc_plan_t* plan,
-                   tc_stream_t stream) {
-  return tc_plan_middle_parts(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, n, u0, u1,
+                   const int32_t* rev_seg, const int64_t* rev_cost, const int32_t* pool, int32_t pool_padded,
+                   int64_t n, int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
+                   tc_plan_t* plan, tc_stream_t stream) {
+  return tc_plan_middle_parts(tab_indptr, tab_indices, rev_indptr, rev_seg, rev_cost, pool, pool_padded, n, u0, u1,
                               bucket_bounds, nbuckets, 1, plan, stream);
 }
 

@@ -45,12 +45,12 @@ __global__ void k_entry_u(const int64_t* __restrict__ rev_indptr, int64_t u0, in
     for (int64_t j = rev_indptr[u] + lane; j < rev_indptr[u + 1]; j += 32) uarr[j - r0] = (int32_t)u;
 }
 
-__global__ void k_tile_keys(const int2* __restrict__ rev_seg, const int64_t* __restrict__ eff_indptr, int64_t n,
+__global__ void k_tile_keys(const int2* __restrict__ rev_seg, const int64_t* __restrict__ pool_indptr, int64_t n,
                             const int32_t* __restrict__ uarr, int64_t r0,
                             int64_t E, const int64_t* __restrict__ vt, int T, int64_t u0, int bu,
                             unsigned long long* keys, int32_t* vals) {
   GRID_STRIDE(i, E) {
-    int64_t v = row_of_edge(eff_indptr, n, (int64_t)rev_seg[r0 + i].x - 1);
+    int64_t v = row_of_edge(pool_indptr, n, (int64_t)rev_seg[r0 + i].x - 1);
     int lo = 0, hi = T;  // largest t with vt[t] <= v
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
@@ -109,7 +109,7 @@ static void excl_sum(Scratch& sc, In in, Out out, int64_t n, cudaStream_t s) {
   TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, s));
 }
 
-static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
+static void tile_pull(const int64_t* eff_indptr, const int64_t* pool_indptr, int64_t n, const int64_t* rev_indptr,
                       const int32_t* rev_seg, int64_t u0, int64_t u1, int64_t tile_ids, int32_t* owner_u,
                       int64_t* owner_ptr, int32_t* segs, int64_t* cost_prefix, int64_t* k_host,
                       int64_t* ntiles_host, cudaStream_t s) {
@@ -144,7 +144,7 @@ static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_i
   auto* kb = sc.alloc<unsigned long long>(E);
   int32_t* va = sc.alloc<int32_t>(E);
   int32_t* vb = sc.alloc<int32_t>(E);
-  k_tile_keys<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(reinterpret_cast<const int2*>(rev_seg), eff_indptr, n, uarr, r0, E, vt, T, u0, bu, ka, va);
+  k_tile_keys<<<grid_for(E, 256, sms * 16), 256, 0, s>>>(reinterpret_cast<const int2*>(rev_seg), pool_indptr, n, uarr, r0, E, vt, T, u0, bu, ka, va);
   check_launch();
   {
     cub::DoubleBuffer<unsigned long long> dk(ka, kb);
@@ -185,12 +185,12 @@ static void tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_i
 
 }  // namespace tcb
 
-extern "C" int tc_tile_pull(const int64_t* eff_indptr, int64_t n, const int64_t* rev_indptr,
+extern "C" int tc_tile_pull(const int64_t* eff_indptr, const int64_t* pool_indptr, int64_t n, const int64_t* rev_indptr,
                             const int32_t* rev_seg, int64_t u0, int64_t u1,
                             int64_t tile_ids, int32_t* owner_u, int64_t* owner_ptr, int32_t* segs,
                             int64_t* cost_prefix, int64_t* k_host, int64_t* ntiles_host, tc_stream_t stream) {
   return tcb::guarded([&] {
-    tcb::tile_pull(eff_indptr, n, rev_indptr, rev_seg, u0, u1, tile_ids, owner_u, owner_ptr, segs,
+    tcb::tile_pull(eff_indptr, pool_indptr, n, rev_indptr, rev_seg, u0, u1, tile_ids, owner_u, owner_ptr, segs,
                    cost_prefix, k_host, ntiles_host, (cudaStream_t)stream);
   });
 }

@@ -123,7 +123,7 @@ class DeviceOps:
                                             shard.indptr)
             h = ctypes.c_void_p()
             L.call("tc_plan_middle", L.ptr(shard.indptr), L.ptr(pool), L.ptr(row), L.ptr(rsegs), L.ptr(cost),
-                   L.ptr(pool), nloc, 0, nloc, None, 1, ctypes.byref(h), L.stream())
+                   L.ptr(pool), 0, nloc, 0, nloc, None, 1, ctypes.byref(h), L.stream())
             plan = shard.cache["surrogate_local"] = _PlanHandle(h, (pool, row, rsegs, cost))
         return plan
 
@@ -202,7 +202,7 @@ class DeviceOps:
         row, rsegs, cost = idx
         out = torch.empty(1, dtype=torch.int64, device=dev)
         L.call("tc_count_middle", L.ptr(indptr), L.ptr(pool), L.ptr(row), L.ptr(rsegs), L.ptr(cost), L.ptr(pool),
-               n_rows, 0, n_rows, None, 1, L.ptr(out), L.stream())
+               0, n_rows, 0, n_rows, None, 1, L.ptr(out), L.stream())
         return int(out.item())
 
 class _PlanHandle:

@@ -25,6 +25,7 @@ import torch
 from . import _lib
 
 _I32_MAX = 2**31 - 1
+POOL_HEAD = 512  # TC_POOL_HEAD (include/tcb200.h)
 
 
 def _as_device_pairs(edges, dev):
@@ -86,16 +87,20 @@ class Graph:
     (graph.py:36-73).  Array fields are torch tensors on the GPU."""
 
     __slots__ = ("n", "m", "eff_indptr", "eff_indices", "relabel", "orig_ids", "deg", "eff_deg",
-                 "_rev_indptr", "_rev_seg", "_rev_cost", "_full", "_cache")
+                 "_rev_indptr", "_rev_seg", "_rev_cost", "_pool_indptr", "_pool", "_full", "_cache")
 
     def __init__(self, n, m, eff_indptr, eff_indices, relabel, orig_ids, deg, eff_deg, rev_indptr,
-                 rev_seg, rev_cost):
+                 rev_seg, rev_cost, pool_indptr, pool):
         self.n, self.m = int(n), int(m)
         self.eff_indptr, self.eff_indices = eff_indptr, eff_indices
         self.relabel, self.orig_ids, self.deg, self.eff_deg = relabel, orig_ids, deg, eff_deg
         # reverse CSR for the pull engine: per u, the (start, end) int32 pairs of
-        # its predecessors' suffixes in eff_indices (rows unordered)
+        # its predecessors' suffixes in _pool coordinates (rows unordered)
         self._rev_indptr, self._rev_seg, self._rev_cost = rev_indptr, rev_seg, rev_cost
+        # the engine's row-padded copy of the forward lists (rows at multiples
+        # of 4 ids, INT32_MAX padding, POOL_HEAD INT32_MAX ids before _pool[0]);
+        # rev_seg's coordinates index it
+        self._pool_indptr, self._pool = pool_indptr, pool
         self._full = None
         self._cache = {}
 
@@ -106,7 +111,8 @@ class Graph:
             fip = torch.empty(self.n + 1, dtype=torch.int64, device=dev)
             fix = torch.empty(max(2 * self.m, 1), dtype=torch.int32, device=dev)
             _lib.call("tc_build_full", _lib.ptr(self.eff_indptr), _lib.ptr(self.eff_indices),
-                      _lib.ptr(self._rev_indptr), _lib.ptr(self._rev_seg), self.n, _lib.ptr(fip),
+                      _lib.ptr(self._rev_indptr), _lib.ptr(self._rev_seg), _lib.ptr(self._pool_indptr), self.n,
+                      _lib.ptr(fip),
                       _lib.ptr(fix), _lib.stream())
             self._full = (fip, fix[: 2 * self.m])
         return self._full
@@ -179,7 +185,7 @@ def tiled_index(g: "Graph", u0: int, u1: int) -> TiledIndex:
         cost = torch.empty(E + 1, dtype=torch.int64, device=dev)
         k, nt = ctypes.c_int64(), ctypes.c_int64()
         if g.n:
-            _lib.call("tc_tile_pull", _lib.ptr(g.eff_indptr), g.n, _lib.ptr(g._rev_indptr),
+            _lib.call("tc_tile_pull", _lib.ptr(g.eff_indptr), _lib.ptr(g._pool_indptr), g.n, _lib.ptr(g._rev_indptr),
                       _lib.ptr(g._rev_seg), u0, u1, TILE_IDS, _lib.ptr(owner_u), _lib.ptr(owner_ptr),
                       _lib.ptr(segs), _lib.ptr(cost), ctypes.byref(k), ctypes.byref(nt), _lib.stream())
         else:
@@ -241,6 +247,9 @@ def _assemble(raw: RawGraph, order) -> Graph:
     eff_indptr, eff_indices = i64(n + 1), i32(m + 4)
     relabel, orig_ids, deg, eff_deg = i32(n), i32(n), i32(n), i32(n)
     rev_indptr, rev_seg, rev_cost = i64(n + 1), i32(2 * m), i64(n + 1)
+    pool_indptr = i64(n + 1)
+    pool_buf = i32(POOL_HEAD + m + 3 * n + 4)  # +4: never an empty view (data_ptr would be NULL)
+    pool = pool_buf[POOL_HEAD:]
     order_t = None
     if order is not None:
         order_t = torch.as_tensor(np.asarray(order, dtype=np.int32)).to(dev).contiguous()
@@ -248,9 +257,10 @@ def _assemble(raw: RawGraph, order) -> Graph:
     _lib.call("tc_build_graph" if hint is None else "tc_build_graph_deg", _lib.ptr(e), m, n,
               _lib.ptr(order_t if hint is None else hint), _lib.ptr(eff_indptr),
               _lib.ptr(eff_indices), _lib.ptr(relabel), _lib.ptr(orig_ids), _lib.ptr(deg),
-              _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_seg), _lib.ptr(rev_cost), _lib.stream())
+              _lib.ptr(eff_deg), _lib.ptr(rev_indptr), _lib.ptr(rev_seg), _lib.ptr(rev_cost), _lib.ptr(pool_indptr),
+              _lib.ptr(pool), _lib.stream())
     g = Graph(n, m, eff_indptr[: n + 1], eff_indices[:m], relabel[:n], orig_ids[:n], deg[:n],
-              eff_deg[:n], rev_indptr[: n + 1], rev_seg[: 2 * m], rev_cost[: n + 1])
+              eff_deg[:n], rev_indptr[: n + 1], rev_seg[: 2 * m], rev_cost[: n + 1], pool_indptr[: n + 1], pool)
     if TILE_IDS:
         tiled_index(g, 0, n)  # optional L2-tiled predecessor index, built with the graph
     return g

@@ -49,7 +49,7 @@ class _MiddlePlan:
 
         h = ctypes.c_void_p()
         _lib.call("tc_plan_middle_parts", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(g._rev_indptr),
-                  _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost), _lib.ptr(g.eff_indices), g.n, u0, u1, None, 1,
+                  _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost), _lib.ptr(g._pool), 1, g.n, u0, u1, None, 1,
                   int(parts), ctypes.byref(h), _lib.stream())
         self.handle = h
 
@@ -81,7 +81,7 @@ def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
     if tiled:
         t = tiled_index(g, int(u0), int(u1))
         _lib.call("tc_count_owners", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), _lib.ptr(t.owner_u),
-                  _lib.ptr(t.owner_ptr), _lib.ptr(t.segs), _lib.ptr(t.cost), _lib.ptr(g.eff_indices), t.k,
+                  _lib.ptr(t.owner_ptr), _lib.ptr(t.segs), _lib.ptr(t.cost), _lib.ptr(g._pool), t.k,
                   _lib.ptr(bounds), k, _lib.ptr(out), 1, _lib.stream())
         return out
     if bounds is None:  # repeated counts of one graph reuse the engine plan
@@ -93,7 +93,7 @@ def count_middle(g: Graph, u0=0, u1=None, bounds=None, out=None, tiled=None):
         return out
     _lib.call("tc_count_middle", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices),
               _lib.ptr(g._rev_indptr), _lib.ptr(g._rev_seg), _lib.ptr(g._rev_cost),
-              _lib.ptr(g.eff_indices), g.n, int(u0), int(u1), _lib.ptr(bounds), k, _lib.ptr(out),
+              _lib.ptr(g._pool), 1, g.n, int(u0), int(u1), _lib.ptr(bounds), k, _lib.ptr(out),
               _lib.stream())
     return out
 

@@ -95,7 +95,7 @@ def count_segments(tab_indptr, tab_indices, pool, owner, segs, nseg, n_owner, bo
     k = 1 if bounds is None else int(bounds.numel()) - 1
     out = torch.empty(k, dtype=torch.int64, device=dev)
     _lib.call("tc_count_middle", _lib.ptr(tab_indptr), _lib.ptr(tab_indices), _lib.ptr(row),
-              _lib.ptr(rsegs), _lib.ptr(cost), _lib.ptr(pool), int(n_owner), 0, int(n_owner),
+              _lib.ptr(rsegs), _lib.ptr(cost), _lib.ptr(pool), 0, int(n_owner), 0, int(n_owner),
               _lib.ptr(bounds), k, _lib.ptr(out), _lib.stream())
     return int(out.sum().item()) if bounds is None else out
 
