@@ -251,6 +251,10 @@ def main():
     ap.add_argument("--other-configs", default="cfg3,cfg5,cfg4",
                     help="N=1: also measure these BASELINE configs (engine, roofline, cold count, e2e; GPU arm "
                          "only) into the line's other_configs; '' to skip")
+    ap.add_argument("--partitioned", default="cfg5,cfg4",
+                    help="N>1: also run these configs through the sharded space-efficient scheme (sharded.py: "
+                         "distributed build, node-range shards, bounded-round list exchange) into 'partitioned'")
+    ap.add_argument("--partition-cost", default="engine", choices=["predsum", "engine"])
     ap.add_argument("--mode", default="replicated", choices=["replicated", "surrogate", "direct"],
                     help="N>1: replicated graph, the engine's chunk plan interleaved across ranks (default), the paper's "
                          "non-overlapping partition with surrogate list exchange, or the direct scheme as a "
@@ -339,8 +343,9 @@ def golden_T(cfg):
                 d = json.load(f)
         except OSError:
             continue
-        if cfg in d and "T" in d[cfg]:
-            return int(d[cfg]["T"]), name
+        for key in d:
+            if (key == cfg or key.startswith(cfg + "_")) and "T" in d[key]:
+                return int(d[key]["T"]), f"tests/golden/{name}:{key}"
     return None, None
 
 
@@ -434,6 +439,78 @@ def other_config(cfg, steps, warmup, flush):
             "traffic_frac": rl["traffic_frac"],
             "e2e_ms": statistics.median(e2e), "e2e_edges_per_s": m / (statistics.median(e2e) / 1e3),
             "e2e_h2d_bytes": m_raw * 8}
+
+
+def device_raw_edges(cfg):
+    """The workload's raw pairs generated on the device (the sharded runs
+    slice them: rank r keeps pairs [r m / N, (r+1) m / N))."""
+    import torch
+
+    c = CONFIGS[cfg]
+    if c["kind"] == "pa":
+        return host_raw_edges(cfg, pin=False).cuda()
+    if c["kind"] == "er":
+        from paper_1406_5687_b200.graph_io import er_edges
+        return er_edges(c["n"], c["m"], c["seed"])
+    if c["kind"] == "cl":
+        from paper_1406_5687_b200.graph_io import chung_lu_edges
+        return chung_lu_edges(c["n"], c["mean"], c["gamma"], c["wmax"], c["seed"])
+    from paper_1406_5687_b200.graph_io import rmat_edges
+    return rmat_edges(c["scale"], c["ef"], c["seed"])
+
+
+def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_words=1 << 27):
+    """The paper's space-efficient scheme end to end on N GPUs (sharded.py):
+    each rank keeps only its slice of the raw pairs, builds only its node
+    range (distributed normalize + build_graph), and the count exchanges
+    suffix lists in bounded rounds; device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1406_5687_b200 import sharded as S
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    raw = device_raw_edges(cfg)
+    m_raw = int(raw.shape[0])
+    sl, base = S.slice_of(raw, world, rank)
+    sl = sl.contiguous().clone()
+    del raw
+    torch.cuda.empty_cache()
+    builds = []
+    sh = None
+    for i in range(2):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        sh = S.build_sharded(sl, base, cost=cost)
+        e.record()
+        torch.cuda.synchronize()
+        builds.append(s.elapsed_time(e))
+    del sl
+    torch.cuda.empty_cache()
+    for _ in range(warmup):
+        T, met = S.count_sharded(sh, round_words=round_words)
+    times = []
+    for _ in range(steps):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        T, met = S.count_sharded(sh, round_words=round_words)
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    ms = max_over_ranks(statistics.median(times))
+    bms = max_over_ranks(min(builds))
+    res = max_over_ranks(float(sh.resident_bytes()))
+    want, src = golden_T(cfg)
+    out = {"workload": CONFIGS[cfg]["desc"], "n": sh.n, "m": sh.m, "m_raw": m_raw, "n_gpus": world,
+           "mode": f"sharded surrogate ({cost} partition)", "triangles": T, "triangles_golden": want,
+           "triangles_ok": (want == T) if want is not None else None, "count_ms": ms,
+           "edges_per_s": sh.m / (ms / 1e3), "build_ms": bms, "max_rank_resident_bytes": res,
+           "rank_partial": met.triangles, "round_words": round_words}
+    del sh
+    torch.cuda.empty_cache()
+    return out
 
 
 def _gpu_arm_core(args):
@@ -575,6 +652,14 @@ def _gpu_arm_core(args):
     torch.cuda.empty_cache()
 
     clock_summary = clocks.summary()
+    partitioned = []
+    if distp and args.partitioned:
+        for pc in [c for c in args.partitioned.split(",") if c]:
+            try:
+                partitioned.append(partitioned_config(pc, max(3, min(args.steps, 5)), 2, args.partition_cost,
+                                                      max_over_ranks, barrier))
+            except Exception as exc:  # reported, never required
+                partitioned.append({"workload": pc, "error": repr(exc)})
     others = []
     if rank == 0 and world == 1 and args.other_configs:
         for oc in [c for c in args.other_configs.split(",") if c and c != args.config]:
@@ -622,6 +707,7 @@ def _gpu_arm_core(args):
             "path": "pinned host raw pairs -> normalize (chunked H2D overlapped with its first passes) -> "
                     "build_graph -> count_triangles_seq -> D2H"},
         "other_configs": others,
+        "partitioned": partitioned,
         "gpu_launches": launches,
         "clocks": clock_summary,
     }

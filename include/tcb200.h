@@ -346,6 +346,102 @@ int tc_parse_edge_list(const unsigned char* buf, int64_t nbytes, int32_t* out_pa
                        int64_t* m_host, int64_t* n_host, int64_t* err_line_host, int32_t* err_code_host,
                        int32_t* err_tokens_host, tc_stream_t stream);
 
+/* ---------------------------------------------------- sharded multi-GPU */
+
+/* The per-rank steps of the sharded pipeline (sharded.py): rank r holds
+ * only its slice of the raw pairs, then its hash share of the deduplicated
+ * edges, then the forward lists of its node range -- a distributed
+ * graph.normalize + build_graph (graph.py:76-153) with partition_ranges
+ * (partitioning.py:139-141) and the surrogate exchange of
+ * space_efficient.py:81-144.  The collectives between the steps (all_reduce
+ * of the replicated per-label arrays, all_to_all of edges and lists) are
+ * the caller's (NCCL).  `pairs` are int32 (u, v) pairs. */
+
+/* Smallest / largest label of the rank's raw slice (negative labels are the
+ * caller's ValueError, graph.py:87-88).  Synchronises. */
+int tc_shard_minmax(const int32_t* pairs, int64_t m, int32_t* min_host, int32_t* max_host, tc_stream_t stream);
+/* present uint8[k] (label occurs in a non-self-loop pair) and first int32[k]
+ * (first raveled position 2(pos_base+i)+j, 0x7F7F7F7F if absent) of the
+ * slice; the caller all-reduces them (MAX / MIN) across ranks. */
+int tc_shard_label_scan(const int32_t* pairs, int64_t m, int64_t pos_base, int64_t k, uint8_t* present,
+                        int32_t* first, tc_stream_t stream);
+/* From the global present / first arrays: map int32[k] = the label's
+ * normalized id (identity when the labels are dense, else first-seen
+ * compaction, graph.py:92-99; -1 for absent labels), n = distinct labels.
+ * Synchronises. */
+int tc_shard_relabel_map(const uint8_t* present, const int32_t* first, int64_t k, int32_t* map, int64_t* n_host,
+                         int32_t* dense_host, tc_stream_t stream);
+/* Canonical keys (min << 32 | max) of the mapped non-self-loop pairs
+ * grouped by destination rank hash(key) mod P (the dedup exchange):
+ * keys_out uint64[m], counts_host int64[P].  map NULL = identity.
+ * Synchronises. */
+int tc_shard_keys(const int32_t* pairs, int64_t m, const int32_t* map, int32_t P, uint64_t* keys_out,
+                  int64_t* counts_host, tc_stream_t stream);
+/* Sorted distinct keys (np.unique(axis=0), graph.py:100-102); labels <
+ * 2^key_bits.  out uint64[k].  Synchronises (returns the count). */
+int tc_shard_dedup(const uint64_t* keys, int64_t k, int32_t key_bits, uint64_t* out, int64_t* k_host,
+                   tc_stream_t stream);
+/* deg int32[n] += both endpoints' counts (graph.py:149-151; caller zeroes
+ * and all-reduces). */
+int tc_shard_degrees(const uint64_t* keys, int64_t k, int32_t* deg, tc_stream_t stream);
+/* Canonical order from the global degrees: orig_ids = ids by ascending
+ * (degree, id) (stable, graph.py:152), relabel = its inverse (graph.py:111-112). */
+int tc_shard_order(const int32_t* deg, int64_t n, int32_t* orig_ids, int32_t* relabel, tc_stream_t stream);
+/* Oriented pairs lohi int32[2k] = (min, max) of the relabelled keys
+ * (graph.py:113-116); effdeg int32[n] += out-degree (caller all-reduces). */
+int tc_shard_orient(const uint64_t* keys, int64_t k, const int32_t* relabel, int32_t* lohi, int32_t* effdeg,
+                    tc_stream_t stream);
+/* PRED_SUM contributions (partitioning.py:91): cost[hi] += d^_lo + d^_hi
+ * (int64[n], caller zeroes and all-reduces). */
+int tc_shard_predsum(const int32_t* lohi, int64_t k, const int32_t* effdeg, int64_t* cost, tc_stream_t stream);
+/* Oriented pairs grouped by the owner of lo under bounds int64[P+1]
+ * (owner_of, partitioning.py:134-136): out int32[2k], counts_host int64[P].
+ * Synchronises. */
+int tc_shard_route(const int32_t* lohi, int64_t k, const int64_t* bounds, int32_t P, int32_t* out,
+                   int64_t* counts_host, tc_stream_t stream);
+/* The rank's forward CSR from its routed pairs (lo in [lo, lo + nrow)):
+ * indptr int64[nrow+1] (local offsets), indices int32[k] rows ascending. */
+int tc_shard_csr(const int32_t* lohi, int64_t k, int64_t lo, int64_t nrow, int64_t* indptr, int32_t* indices,
+                 tc_stream_t stream);
+/* Row-padded copy of a CSR for the engine (see tc_build_graph's pool):
+ * pool_indptr int64[nrow+1]; pool int32[TC_POOL_HEAD + indptr[nrow] + 3 nrow + 4]
+ * passed TC_POOL_HEAD ids past its start. */
+int tc_shard_pool(const int64_t* indptr, const int32_t* indices, int64_t nrow, int64_t* pool_indptr, int32_t* pool,
+                  tc_stream_t stream);
+/* Engine cost of the middle-vertex owners (the pull cost of build_graph's
+ * rev_cost): acc uint64[n] += suffix length + seg_weight per predecessor
+ * entry of the local rows (caller zeroes, all-reduces); _fin adds the table term
+ * tab_weight * d^_u + 16 for owners with work (build_graph's rev_cost is
+ * seg_weight 2, tab_weight 1; the partition weights are sharded.py's). */
+int tc_shard_engine_cost(const int64_t* indptr, const int32_t* indices, int64_t nrow, int64_t seg_weight,
+                         uint64_t* acc, tc_stream_t stream);
+int tc_shard_engine_cost_fin(const uint64_t* acc, const int32_t* effdeg, int64_t n, int64_t tab_weight,
+                             int64_t* cost, tc_stream_t stream);
+/* Surrogate send plan (_kernels.py:94-126 LastProc records, one message per
+ * (v, dest > rank) with an id of N^_v owned by dest; the message is row v of
+ * the shard's padded pool from the 16-byte chunk holding its first id >=
+ * bounds[dest] on): sizes_dev int64[3P] = lists, padded words, whole-list
+ * words per destination (the last is the reference's bytes_sent
+ * accounting); copied to sizes_host if not NULL (synchronises).  P <= 32. */
+int tc_shard_send_sizes(const int64_t* indptr, const int32_t* indices, int64_t nrow, const int64_t* pool_indptr,
+                        const int64_t* bounds, int32_t P, int32_t rank, int64_t* sizes_dev, int64_t* sizes_host,
+                        tc_stream_t stream);
+/* The messages, grouped by destination: out_len int32[lists] (ids per
+ * message), out_ids int32[words] (padded rows; 16-byte aligned). */
+int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nrow, const int64_t* pool_indptr,
+                       const int32_t* pool, const int64_t* bounds, int32_t P, int32_t rank, const int64_t* sizes_dev,
+                       int32_t* out_len, int32_t* out_ids, tc_stream_t stream);
+/* Middle-vertex segments of a set of padded rows (row r: row_len[r] ids at
+ * pool_indptr[r], computed here) for owners u in [lo, hi): the suffix of the
+ * row after each u (surrogate_count_list, _kernels.py:70-80), grouped by
+ * owner -- rev_indptr int64[hi-lo+1], rev_seg int32[2*cap], rev_cost
+ * int64[hi-lo+1] (tables tab_indptr indexed u - lo) for tc_plan_middle with
+ * pool_padded = 1.  cap >= the number of row entries.  nseg_host (nullable)
+ * synchronises. */
+int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
+                   const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr, int32_t* rev_seg,
+                   int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream);
+
 /* ------------------------------------------------------------ generators */
 
 /* ER G(n,m) raw pairs (configs 1, 5): out int32[2m]. */

@@ -56,6 +56,23 @@ _SIGS = {
     "tc_surrogate_pack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_owner_segments": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _pi64, _vp],
     "tc_segments_csr": [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
+    "tc_shard_minmax": [_vp, _i64, ctypes.POINTER(_i32), ctypes.POINTER(_i32), _vp],
+    "tc_shard_label_scan": [_vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "tc_shard_relabel_map": [_vp, _vp, _i64, _vp, _pi64, ctypes.POINTER(_i32), _vp],
+    "tc_shard_keys": [_vp, _i64, _vp, _i32, _vp, _vp, _vp],
+    "tc_shard_dedup": [_vp, _i64, _i32, _vp, _pi64, _vp],
+    "tc_shard_degrees": [_vp, _i64, _vp, _vp],
+    "tc_shard_order": [_vp, _i64, _vp, _vp, _vp],
+    "tc_shard_orient": [_vp, _i64, _vp, _vp, _vp, _vp],
+    "tc_shard_predsum": [_vp, _i64, _vp, _vp, _vp],
+    "tc_shard_route": [_vp, _i64, _vp, _i32, _vp, _vp, _vp],
+    "tc_shard_csr": [_vp, _i64, _i64, _i64, _vp, _vp, _vp],
+    "tc_shard_pool": [_vp, _vp, _i64, _vp, _vp, _vp],
+    "tc_shard_engine_cost": [_vp, _vp, _i64, _i64, _vp, _vp],
+    "tc_shard_engine_cost_fin": [_vp, _vp, _i64, _i64, _vp, _vp],
+    "tc_shard_send_sizes": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
+    "tc_shard_send_pack": [_vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
+    "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
     "tc_parse_edge_list": [_vp, _i64, _vp, _i64, _pi64, _pi64, _pi64, ctypes.POINTER(ctypes.c_int32),
                            ctypes.POINTER(ctypes.c_int32), _vp],
     "tc_gen_er": [_i64, _i64, _u64, _vp, _vp],

@@ -49,6 +49,14 @@ def test_nccl_world1_schemes(nccl_group):
     c = count_middle_part(g, 0, 1)  # bench.py's replicated step at world size 1
     dist.all_reduce(c)
     assert int(c.item()) == T
+    # the sharded space-efficient pipeline: distributed build + bounded-round count
+    from paper_1406_5687_b200.sharded import build_sharded, count_sharded
+    for cost in ("predsum", "engine"):
+        sh = build_sharded(raw.contiguous(), 0, cost=cost)
+        assert sh.n == g.n and sh.m == g.m
+        assert torch.equal(sh.indices, g.eff_indices) and torch.equal(sh.indptr, g.eff_indptr)
+        total, met = count_sharded(sh, round_words=1024)
+        assert total == T and met.triangles == T
 
 
 @pytest.mark.parametrize("mode", ["replicated", "surrogate", "direct"])
@@ -66,10 +74,14 @@ def test_bench_multi_gpu_path_world1(mode, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(repo, "bench.py"),
            "--gpus", "1", "--steps", "2", "--warmup", "3", "--mode", mode, "--no-e2e", "--no-cpu-baseline",
-           "--config", "cfg1"]
+           "--config", "cfg1", "--partitioned", "cfg1" if mode == "replicated" else ""]
     out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["workload_detail"]["triangles"] == 722 and line["n_gpus"] == 1
     assert {"replicated": "replicated", "surrogate": "surrogate", "direct": "pull"}[mode] in \
         line["workload_detail"]["parallelism"]
+    if mode == "replicated":  # the sharded space-efficient scheme through NCCL (sharded.py)
+        part = line["partitioned"][0]
+        assert part.get("error") is None, part
+        assert part["triangles"] == 722 and part["triangles_ok"] and part["n_gpus"] == 1

@@ -1,0 +1,160 @@
+"""The sharded multi-GPU pipeline (paper_1406_5687_b200/sharded.py): a
+distributed normalize + build_graph where each rank keeps only its node
+range, and the surrogate count over bounded exchange rounds.
+
+CPU: the protocol with the numpy per-rank steps (tests/dist_helpers.py),
+emulated in one process and over gloo at world size 2 / 3.  GPU: the
+device steps (csrc/shard.cu) emulated rank by rank on one B200.  Every case
+is checked against the reference's own outputs (tests/golden): each rank's
+forward lists equal the reference graph's rows of its range, the PRED_SUM
+bounds equal partition_ranges, the rank partials / census / bytes_sent equal
+count_space_surrogate's metrics, and the total equals T."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import SMALL
+from dist_helpers import NumpyShardOps
+from paper_1406_5687_b200 import sharded as S
+
+CASES = ["er_60_0.2_21", "pa_500_8_11", "sparse_labels", "gnm_2000_16000"]
+
+
+def _check_build(case, shards, P):
+    assert shards[0].bounds.tolist() == case[f"bounds_predsum_{P}"].tolist()
+    ip, ix = case["eff_indptr"], case["eff_indices"]
+    for sh in shards:
+        lo, hi = sh.lo, sh.hi
+        assert sh.n == len(case["relabel"]) and sh.m == len(ix)
+        assert np.array_equal(sh.indptr.cpu().numpy(), ip[lo: hi + 1] - ip[lo])
+        assert np.array_equal(sh.indices.cpu().numpy(), ix[ip[lo]: ip[hi]])
+        if sh.relabel is not None:
+            assert np.array_equal(sh.relabel.cpu().numpy(), case["relabel"])
+            assert np.array_equal(sh.orig_ids.cpu().numpy(), case["orig_ids"])
+
+
+def _check_count(case, tot, mets, P):
+    assert tot == int(case["T"][0])
+    assert [m.triangles for m in mets] == case[f"surr_tri_{P}"].tolist()
+    assert np.stack([m.data_msgs_to for m in mets]).tolist() == case[f"surr_census_{P}"].tolist()
+    assert [m.bytes_sent for m in mets] == case[f"surr_bytes_{P}"].tolist()
+    assert [m.data_msgs_sent for m in mets] == case[f"surr_msgs_{P}"].tolist()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_sharded_protocol_emulated_numpy(name):
+    case = SMALL[name]
+    raw = torch.as_tensor(case["raw"].astype(np.int32))
+    ops = NumpyShardOps()
+    for P in (2, 3):
+        shards, _ = S.emulate_build(raw, P, ops=ops, keep_maps=True)
+        _check_build(case, shards, P)
+        for rw in (8, 1 << 27):  # many small rounds / one round
+            tot, mets, _ = S.emulate_count(shards, ops=ops, round_words=rw)
+            _check_count(case, tot, mets, P)
+        eshards, _ = S.emulate_build(raw, P, cost="engine", ops=ops)
+        assert sum(sh.m_local for sh in eshards) == len(case["eff_indices"])
+        assert S.emulate_count(eshards, ops=ops)[0] == int(case["T"][0])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, cost, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from conftest import SMALL as SM
+    from dist_helpers import NumpyShardOps as Ops
+    from paper_1406_5687_b200 import sharded as SS
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        case = SM[name]
+        raw = torch.as_tensor(case["raw"].astype(np.int32))
+        sl, base = SS.slice_of(raw, world, rank)
+        sh = SS.build_sharded(sl.contiguous(), base, cost=cost, ops=Ops(), keep_maps=True)
+        tot, met = SS.count_sharded(sh, ops=Ops(), round_words=16)
+        q.put((rank, sh.lo, sh.hi, sh.bounds.tolist(), sh.indptr.numpy().tolist(), sh.indices.numpy().tolist(),
+               tot, met.triangles, met.data_msgs_to.tolist(), met.bytes_sent, met.data_msgs_sent))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["pa_500_8_11", "sparse_labels"])
+@pytest.mark.parametrize("cost", ["predsum", "engine"])
+def test_sharded_gloo(name, world, cost):
+    case = SMALL[name]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, cost, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ip, ix = case["eff_indptr"], case["eff_indices"]
+    T = int(case["T"][0])
+    for rank, lo, hi, bounds, sip, six, tot, tri, to, bts, sent in res:
+        assert tot == T
+        assert np.array_equal(np.asarray(sip), ip[lo: hi + 1] - ip[lo])
+        assert np.array_equal(np.asarray(six, np.int64), ix[ip[lo]: ip[hi]])
+        if cost == "predsum":
+            assert bounds == case[f"bounds_predsum_{world}"].tolist()
+            assert tri == int(case[f"surr_tri_{world}"][rank])
+            assert to == case[f"surr_census_{world}"][rank].tolist()
+            assert bts == int(case[f"surr_bytes_{world}"][rank])
+            assert sent == int(case[f"surr_msgs_{world}"][rank])
+    # the ranges tile [0, n)
+    assert res[0][1] == 0 and res[-1][2] == len(case["relabel"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_sharded_device_emulated(name):
+    """The device steps (csrc/shard.cu) for every fixture at P = 2, 3, 5, 8."""
+    case = SMALL[name]
+    if "bounds_predsum_2" not in case:
+        pytest.skip("fixture without partition goldens")
+    raw = torch.as_tensor(case["raw"].astype(np.int32)).cuda()
+    for P in (2, 3, 5, 8):
+        if f"surr_tri_{P}" not in case:
+            continue
+        shards, _ = S.emulate_build(raw, P, keep_maps=True)
+        _check_build(case, shards, P)
+        for rw in (64, 1 << 27):
+            tot, mets, _ = S.emulate_count(shards, round_words=rw)
+            _check_count(case, tot, mets, P)
+        eshards, _ = S.emulate_build(raw, P, cost="engine")
+        assert S.emulate_count(eshards)[0] == int(case["T"][0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_device_cfg2(configs, P):
+    """cfg 2 (PA n = 10^6, 50 M edges) at full size: the reference's PRED_SUM
+    bounds, surrogate partials and census, per rank."""
+    import bench
+
+    c = configs["cfg2_pa_1000000_100_seed1"]
+    raw = bench.host_raw_edges("cfg2", pin=False).cuda()
+    shards, _ = S.emulate_build(raw, P)
+    del raw
+    assert shards[0].bounds.tolist() == c[f"bounds_predsum_{P}"]
+    assert sum(sh.m_local for sh in shards) == c["m"]
+    tot, mets, _ = S.emulate_count(shards, round_words=1 << 22)
+    assert tot == c["T"]
+    assert [m.triangles for m in mets] == c[f"surr_tri_{P}"]
+    assert np.stack([m.data_msgs_to for m in mets]).tolist() == c[f"surr_census_{P}"]
