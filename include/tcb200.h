@@ -411,12 +411,14 @@ int tc_shard_pool(const int64_t* indptr, const int32_t* indices, int64_t nrow, i
 /* Engine cost of the middle-vertex owners (the pull cost of build_graph's
  * rev_cost): acc uint64[n] += suffix length + seg_weight per predecessor
  * entry of the local rows (caller zeroes, all-reduces); _fin adds the table term
- * tab_weight * d^_u + 16 for owners with work (build_graph's rev_cost is
- * seg_weight 2, tab_weight 1; the partition weights are sharded.py's). */
+ * tab_weight * d^_u + 16 for owners with work, and send_weight * d^_v for
+ * every node (its list's share of the surrogate send) (build_graph's
+ * rev_cost is seg_weight 2, tab_weight 1, send_weight 0; the partition
+ * weights are sharded.py's). */
 int tc_shard_engine_cost(const int64_t* indptr, const int32_t* indices, int64_t nrow, int64_t seg_weight,
                          uint64_t* acc, tc_stream_t stream);
 int tc_shard_engine_cost_fin(const uint64_t* acc, const int32_t* effdeg, int64_t n, int64_t tab_weight,
-                             int64_t* cost, tc_stream_t stream);
+                             int64_t send_weight, int64_t* cost, tc_stream_t stream);
 /* Surrogate send plan (_kernels.py:94-126 LastProc records, one message per
  * (v, dest > rank) with an id of N^_v owned by dest; the message is row v of
  * the shard's padded pool from the 16-byte chunk holding its first id >=

@@ -238,10 +238,10 @@ __global__ void k_sh_engine_cost(const int64_t* __restrict__ indptr, const int32
 }
 
 __global__ void k_sh_engine_cost_fin(const unsigned long long* __restrict__ acc, const int32_t* __restrict__ effdeg,
-                                     int64_t n, int64_t tab_weight, int64_t* cost) {
+                                     int64_t n, int64_t tab_weight, int64_t send_weight, int64_t* cost) {
   GRID_STRIDE(u, n) {
     const int64_t d = effdeg[u];
-    cost[u] = (d > 0 && acc[u] > 0) ? (int64_t)acc[u] + tab_weight * d + kTabCostS : 0;
+    cost[u] = ((d > 0 && acc[u] > 0) ? (int64_t)acc[u] + tab_weight * d + kTabCostS : 0) + send_weight * d;
   }
 }
 
@@ -292,44 +292,75 @@ __global__ void k_sh_send_count(const int64_t* __restrict__ indptr, const int32_
   }
 }
 
-// Emit pass: warp per row; the lanes find the row's destinations, then the
-// warp copies each message as 16-byte chunks of the padded pool.  One atomic
-// claims a message's list slot and its words together (list count in the
-// high 26 bits, words in the low 38), so the lengths and the lists agree in
-// order (which is otherwise unspecified; the receiver's count does not
-// depend on it).
+// Emit pass.  A block takes a contiguous run of rows; its warps (one row at
+// a time, lanes = destinations) first total the block's messages per
+// destination in shared memory, one thread claims the block's ranges with
+// one global atomic per destination, and the warps then claim slots inside
+// them and copy each message as 16-byte chunks of the padded pool.  A slot
+// claim is one 64-bit atomic holding the message count (high 26 bits) and
+// its words (low 38), so the lengths and the lists agree in order (which is
+// otherwise unspecified; the receiver's count does not depend on it).
+static constexpr int kEmitMaxP = 32;
+__device__ __forceinline__ bool send_dest(const int32_t* __restrict__ ids, int64_t a, int64_t d,
+                                          const int64_t* __restrict__ bounds, int lane, int P, int rank, int64_t& s) {
+  s = 0;
+  if (lane <= rank || lane >= P) return false;
+  s = row_lb(ids, a, d, bounds[lane]);
+  return s < row_lb(ids, a, d, bounds[lane + 1]);
+}
+
 __global__ void k_sh_send_emit(const int64_t* __restrict__ indptr, const int32_t* __restrict__ ids, int64_t nrow,
                                const int64_t* __restrict__ pptr, const int4* __restrict__ pool4,
                                const int64_t* __restrict__ bounds, int P, int rank,
                                const long long* __restrict__ list_off, const long long* __restrict__ word_off,
                                unsigned long long* cur, int32_t* out_len, int4* out4) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nrow; v += nw) {
+  __shared__ unsigned long long btot[kEmitMaxP], bcur[kEmitMaxP];
+  __shared__ long long bl[kEmitMaxP], bw[kEmitMaxP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int64_t per = (nrow + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(nrow, r0 + per);
+  if (threadIdx.x < kEmitMaxP) {
+    btot[threadIdx.x] = 0;
+    bcur[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  for (int64_t v = r0 + warp; v < r1; v += nwarp) {  // block totals
     const int64_t a = indptr[v], d = indptr[v + 1] - a;
     if (d == 0) continue;
-    int64_t s = 0;
-    bool hit = false;
-    if (lane > rank && lane < P) {
-      s = row_lb(ids, a, d, bounds[lane]);
-      hit = s < row_lb(ids, a, d, bounds[lane + 1]);
+    int64_t s;
+    if (send_dest(ids, a, d, bounds, lane, P, rank, s)) {
+      const int64_t nch = ((pptr[v + 1] - pptr[v]) >> 2) - (s >> 2);
+      atomicAdd(&btot[lane], (1ull << 38) + (unsigned long long)(4 * nch));
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < P && btot[threadIdx.x]) {  // the block's ranges
+    const unsigned long long old = atomicAdd(&cur[threadIdx.x], btot[threadIdx.x]);
+    bl[threadIdx.x] = list_off[threadIdx.x] + (long long)(old >> 38);
+    bw[threadIdx.x] = word_off[threadIdx.x] + (long long)(old & ((1ull << 38) - 1));
+  }
+  __syncthreads();
+  for (int64_t v = r0 + warp; v < r1; v += nwarp) {
+    const int64_t a = indptr[v], d = indptr[v + 1] - a;
+    if (d == 0) continue;
+    int64_t s;
+    const bool hit = send_dest(ids, a, d, bounds, lane, P, rank, s);
     unsigned todo = __ballot_sync(0xffffffffu, hit);
     const int64_t p0 = pptr[v] >> 2, pd = (pptr[v + 1] - pptr[v]) >> 2;  // in chunks
+    long long li = 0, wi = 0;
+    if (hit) {  // lane j claims this row's slot in destination j's block range
+      const int64_t nch = pd - (s >> 2);
+      const unsigned long long old = atomicAdd(&bcur[lane], (1ull << 38) + (unsigned long long)(4 * nch));
+      li = bl[lane] + (long long)(old >> 38);
+      wi = bw[lane] + (long long)(old & ((1ull << 38) - 1));
+      out_len[li] = (int32_t)(d - 4 * (s >> 2));
+    }
     while (todo) {
       const int jj = __ffs(todo) - 1;
       todo &= todo - 1;
       const int64_t c0 = __shfl_sync(0xffffffffu, s, jj) >> 2;  // first chunk of the message
-      const int64_t nch = pd - c0;
-      long long wi = 0;
-      if (lane == 0) {
-        const unsigned long long old = atomicAdd(&cur[jj], (1ull << 38) + (unsigned long long)(4 * nch));
-        const long long li = list_off[jj] + (long long)(old >> 38);
-        wi = word_off[jj] + (long long)(old & ((1ull << 38) - 1));
-        out_len[li] = (int32_t)(d - 4 * c0);
-      }
-      wi = __shfl_sync(0xffffffffu, wi, 0) >> 2;
-      for (int64_t c = lane; c < nch; c += 32) out4[wi + c] = __ldg(&pool4[p0 + c0 + c]);
+      const int64_t w0 = __shfl_sync(0xffffffffu, wi, jj) >> 2;
+      for (int64_t c = lane; c < pd - c0; c += 32) out4[w0 + c] = __ldg(&pool4[p0 + c0 + c]);
     }
   }
 }
@@ -337,24 +368,45 @@ __global__ void k_sh_send_emit(const int64_t* __restrict__ indptr, const int32_t
 // ------------------------------------------------------------ receive index
 
 // Rows of a padded pool (row r at pptr[r], length len[r]); owners u in
-// [lo, hi).  Pass 1 counts the non-empty suffix segments per owner.
+// [lo, hi).  Pass 1 accumulates, per owner, its non-empty suffix segments
+// and their total length in one 64-bit atomic (count << 40 | length sum);
+// pass 2 scatters the segments with a 32-bit cursor.
+static constexpr int kCntShift = 40;
 __global__ void k_sh_idx_count(const int64_t* __restrict__ pptr, const int32_t* __restrict__ len, int64_t nrow,
-                               const int32_t* __restrict__ pool, int64_t lo, int64_t hi, int32_t* cnt) {
+                               const int32_t* __restrict__ pool, int64_t lo, int64_t hi, unsigned long long* acc) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
     const int64_t p = pptr[r], d = len[r];
     for (int64_t i = lane; i + 1 < d; i += 32) {
       const int32_t u = pool[p + i];
-      if (u >= lo && u < hi) atomicAdd(&cnt[u - lo], 1);
+      if (u >= lo && u < hi)
+        atomicAdd(&acc[u - lo], (1ull << kCntShift) + (unsigned long long)(d - i - 1));
     }
+  }
+}
+
+__global__ void k_sh_idx_rows(const unsigned long long* __restrict__ acc, const int64_t* __restrict__ tab_indptr,
+                              int64_t nx, int64_t* cnt, int64_t* cost) {
+  GRID_STRIDE(x, nx + 1) {
+    if (x == nx) {
+      cnt[x] = 0;
+      cost[x] = 0;
+      continue;
+    }
+    const unsigned long long a = acc[x];
+    const int64_t k = (int64_t)(a >> kCntShift), sum = (int64_t)(a & ((1ull << kCntShift) - 1));
+    const int64_t d = tab_indptr[x + 1] - tab_indptr[x];
+    cnt[x] = k;
+    // the pull-engine cost of build_graph's rev_cost (suffix lengths + 2 per
+    // segment, table d + 16)
+    cost[x] = (d > 0 && k > 0) ? sum + kSegCostS * k + d + kTabCostS : 0;
   }
 }
 
 __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* __restrict__ len, int64_t nrow,
                               const int32_t* __restrict__ pool, int64_t lo, int64_t hi,
-                              const int64_t* __restrict__ rev_indptr, int32_t* cursor, int2* rev_seg,
-                              unsigned long long* acc) {
+                              const int64_t* __restrict__ rev_indptr, int32_t* cursor, int2* rev_seg) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
@@ -364,21 +416,8 @@ __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* _
       if (u >= lo && u < hi) {
         const int64_t x = u - lo;
         rev_seg[rev_indptr[x] + atomicAdd(&cursor[x], 1)] = make_int2((int)(p + i + 1), (int)(p + d));
-        atomicAdd(&acc[x], (unsigned long long)(d - i - 1 + kSegCostS));
       }
     }
-  }
-}
-
-__global__ void k_sh_idx_cost(const unsigned long long* __restrict__ acc, const int64_t* __restrict__ tab_indptr,
-                              int64_t nx, int64_t* cost) {
-  GRID_STRIDE(x, nx + 1) {
-    if (x == nx) {
-      cost[x] = 0;
-      continue;
-    }
-    const int64_t d = tab_indptr[x + 1] - tab_indptr[x];
-    cost[x] = (d > 0 && acc[x] > 0) ? (int64_t)acc[x] + d + kTabCostS : 0;
   }
 }
 
@@ -659,13 +698,13 @@ int tc_shard_engine_cost(const int64_t* indptr, const int32_t* indices, int64_t 
 }
 
 int tc_shard_engine_cost_fin(const uint64_t* acc, const int32_t* effdeg, int64_t n, int64_t tab_weight,
-                             int64_t* cost, tc_stream_t stream) {
+                             int64_t send_weight, int64_t* cost, tc_stream_t stream) {
   return guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
     if (n <= 0) return;
-    TC_REQUIRE(tab_weight >= 0, TC_EINVAL, "negative table weight");
+    TC_REQUIRE(tab_weight >= 0 && send_weight >= 0, TC_EINVAL, "negative weight");
     k_sh_engine_cost_fin<<<grid_for(n, kBlk), kBlk, 0, s>>>(reinterpret_cast<const unsigned long long*>(acc), effdeg, n,
-                                                          tab_weight, cost);
+                                                          tab_weight, send_weight, cost);
     check_launch();
   });
 }
@@ -705,7 +744,7 @@ int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nr
     ex_sum(sc, reinterpret_cast<const long long*>(sizes_dev), off, P, s);
     ex_sum(sc, reinterpret_cast<const long long*>(sizes_dev) + P, off + P, P, s);
     TC_CUDA(cudaMemsetAsync(off + 2 * P, 0, 2 * P * sizeof(long long), s));
-    k_sh_send_emit<<<grid_for(nrow * 32, kBlk, sm_count() * 16), kBlk, 0, s>>>(
+    k_sh_send_emit<<<grid_for(nrow * 32, kBlk, sm_count() * 8), kBlk, 0, s>>>(
         indptr, indices, nrow, pool_indptr, reinterpret_cast<const int4*>(pool), bounds, P, rank, off, off + P,
         reinterpret_cast<unsigned long long*>(off + 2 * P), out_len, reinterpret_cast<int4*>(out_ids));
     check_launch();
@@ -725,27 +764,26 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
     k_sh_len_sizes<<<grid_for(nrow + 1, kBlk), kBlk, 0, s>>>(row_len, nrow, sz);
     check_launch();
     ex_sum(sc, sz, pool_indptr, nrow + 1, s);
-    int32_t* cnt = sc.alloc<int32_t>(nx + 1);
-    TC_CUDA(cudaMemsetAsync(cnt, 0, (nx + 1) * sizeof(int32_t), s));
+    auto* acc = sc.alloc<unsigned long long>(nx + 1);
+    TC_CUDA(cudaMemsetAsync(acc, 0, (nx + 1) * sizeof(unsigned long long), s));
     const int grid = grid_for(std::max<int64_t>(nrow, 1) * 32, kBlk, sm_count() * 16);
     if (nrow > 0) {
-      k_sh_idx_count<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, cnt);
+      k_sh_idx_count<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, acc);
       check_launch();
     }
+    int64_t* cnt = sc.alloc<int64_t>(nx + 1);
+    int64_t* cost = sc.alloc<int64_t>(nx + 1);
+    k_sh_idx_rows<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(acc, tab_indptr, nx, cnt, cost);
+    check_launch();
     ex_sum(sc, cnt, rev_indptr, nx + 1, s);
+    ex_sum(sc, cost, rev_cost, nx + 1, s);
     int32_t* cur = sc.alloc<int32_t>(nx + 1);
-    auto* acc = sc.alloc<unsigned long long>(nx + 1);
     TC_CUDA(cudaMemsetAsync(cur, 0, (nx + 1) * sizeof(int32_t), s));
-    TC_CUDA(cudaMemsetAsync(acc, 0, (nx + 1) * sizeof(unsigned long long), s));
     if (nrow > 0) {
       k_sh_idx_emit<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
-                                          reinterpret_cast<int2*>(rev_seg), acc);
+                                          reinterpret_cast<int2*>(rev_seg));
       check_launch();
     }
-    int64_t* cost = sc.alloc<int64_t>(nx + 1);
-    k_sh_idx_cost<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(acc, tab_indptr, nx, cost);
-    check_launch();
-    ex_sum(sc, cost, rev_cost, nx + 1, s);
     if (nseg_host) *nseg_host = scalar_of(rev_indptr + nx, s);
   });
 }

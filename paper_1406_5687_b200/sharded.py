@@ -57,10 +57,13 @@ POOL_HEAD = 512  # TC_POOL_HEAD (include/tcb200.h)
 # Weight of an owner's table ids against its streamed probe ids in the
 # engine-cost partition (cost="engine"): staging a table costs more per id
 # than a probe (hashing + atomics), see DESIGN.md §4.
-TAB_WEIGHT = int(__import__("os").environ.get("TCB_TAB_WEIGHT", "1"))
+TAB_WEIGHT = int(__import__("os").environ.get("TCB_TAB_WEIGHT", "8"))
 # Weight of a predecessor segment (one list suffix streamed for one owner)
 # against one probe id.
 SEG_WEIGHT = int(__import__("os").environ.get("TCB_SEG_WEIGHT", "2"))
+# Weight of a node's own list (the owner packs and sends it to the ranks
+# above) against one probe id.
+SEND_WEIGHT = int(__import__("os").environ.get("TCB_SEND_WEIGHT", "16"))
 INT32_MAX = 2**31 - 1
 
 
@@ -204,14 +207,19 @@ class ShardOps:
                     int(SEG_WEIGHT), self.L.ptr(acc), self.L.stream())
         return acc[:n]
 
-    def engine_cost(self, acc, effdeg, n, tab_weight=1):
+    def engine_cost(self, acc, effdeg, n, tab_weight=1, send_weight=0):
         c = torch.empty(max(n, 1), dtype=torch.int64, device=self.dev)
         self.L.call("tc_shard_engine_cost_fin", self.L.ptr(acc), self.L.ptr(effdeg), int(n), int(tab_weight),
-                    self.L.ptr(c), self.L.stream())
+                    int(send_weight), self.L.ptr(c), self.L.stream())
         return c[:n]
 
     # -- count --
     def send_sizes(self, sh, P, rank):
+        # a property of the partitioned graph (like the engine plan): computed
+        # at the first count of a shard
+        hit = sh.cache.get(("send_sizes", P, rank))
+        if hit is not None:
+            return hit
         sizes = torch.empty(3 * P, dtype=torch.int64, device=self.dev)
         host = np.zeros(3 * P, np.int64)
         b = sh.cache.get("bounds_dev")
@@ -220,6 +228,7 @@ class ShardOps:
         self.L.call("tc_shard_send_sizes", self.L.ptr(sh.indptr), self.L.ptr(sh.indices), sh.hi - sh.lo,
                     self.L.ptr(sh.pool_indptr), self.L.ptr(b), int(P), int(rank), self.L.ptr(sizes),
                     host.ctypes.data_as(ctypes.c_void_p), self.L.stream())
+        sh.cache[("send_sizes", P, rank)] = (sizes, host.reshape(3, P))
         return sizes, host.reshape(3, P)
 
     def send_pack(self, sh, P, rank, sizes_dev, nl, nw):
@@ -350,6 +359,14 @@ def run_dist(gen, group=None):
             raise ValueError(f"unknown collective {kind}")
 
 
+def ops_of(gen):
+    """The ops object a rank generator was started with (emulation timing)."""
+    try:
+        return gen.gi_frame.f_locals.get("ops")
+    except AttributeError:
+        return None
+
+
 def emulate(gens, timed=False):
     """Runs P rank generators in lockstep in this process (one device): every
     collective is performed once all ranks have reached it.  With timed=True
@@ -377,6 +394,11 @@ def emulate(gens, timed=False):
                 done[r] = True
                 out[r] = stop.value
             if timed:
+                # the segment's side-stream work (engine runs, planning) is
+                # counted with it: per-rank time is serialised (no overlap
+                # between the exchange and the local engine)
+                for st in getattr(ops_of(gens[r]), "_st", None) or ():
+                    torch.cuda.current_stream().wait_stream(st)
                 e.record()
                 torch.cuda.synchronize()
                 ms[r] += s.elapsed_time(e)
@@ -480,7 +502,7 @@ def build_gen(pairs, pos_base, P, rank, cost="predsum", ops=None, keep_maps=Fals
         # pieces in source-rank order keeps rows ascending)
         acc = ops.engine_cost_acc(indptr, indices, n)
         acc = yield ("allreduce", acc, "sum")
-        ec = ops.engine_cost(acc, effdeg, n, TAB_WEIGHT)
+        ec = ops.engine_cost(acc, effdeg, n, TAB_WEIGHT, SEND_WEIGHT)
         del acc
         nb = ops.balanced(ec, n, P)
         del ec
@@ -549,35 +571,43 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
     met.data_msgs_sent = int(lists.sum())
     met.completion_msgs_sent = P - 1
     met.bytes_sent = WORD_BYTES * (2 * int(lists.sum()) + int(full.sum()) + (P - 1))
-    st = torch.as_tensor(np.stack([lists, words], 1).astype(np.int64)).to(dev)
-    rsz, _ = yield ("a2a", st, np.ones(P, np.int64))
-    rsz = rsz.cpu().numpy() if isinstance(rsz, torch.Tensor) else np.asarray(rsz)
-    rlists, rwords = rsz[:, 0], rsz[:, 1]
-    tp = _phase(prof, "sizes", tp)
+    xkey = ("xplan", P, rank, round_words)
+    xplan = sh.cache.get(xkey) if hasattr(sh, "cache") else None
+    if xplan is None:
+        # what every peer sends here, and the round structure: static for a
+        # partitioned graph, exchanged at its first count
+        st = torch.as_tensor(np.stack([lists, words], 1).astype(np.int64)).to(dev)
+        rsz, _ = yield ("a2a", st, np.ones(P, np.int64))
+        rsz = rsz.cpu().numpy() if isinstance(rsz, torch.Tensor) else np.asarray(rsz)
+        rlists, rwords = rsz[:, 0], rsz[:, 1]
+        # rounds over peer distance t: sends to rank + t, receives from
+        # rank - t; a round closes once the largest receive volume (over
+        # ranks) would pass round_words -- the same grouping on every rank
+        vol = torch.zeros(P, dtype=torch.int64, device=dev)
+        for t in range(1, P):
+            if rank - t >= 0:
+                vol[t] = int(rwords[rank - t])
+        vol = yield ("allreduce", vol, "max")
+        vol = vol.cpu().numpy()
+        rounds, cur, acc = [], [], 0
+        for t in range(1, P):
+            w = int(vol[t])
+            if cur and acc + w > round_words:
+                rounds.append(cur)
+                cur, acc = [], 0
+            cur.append(t)
+            acc += w
+        if cur:
+            rounds.append(cur)
+        xplan = (rlists, rwords, rounds)
+        if hasattr(sh, "cache"):
+            sh.cache[xkey] = xplan
+    rlists, rwords, rounds = xplan
     lens, ids = ops.send_pack(sh, P, rank, sizes_dev, int(lists.sum()), int(words.sum()))
     tp = _phase(prof, "pack", tp)
     loff = np.concatenate([[0], np.cumsum(lists)])
     woff = np.concatenate([[0], np.cumsum(words)])
     met.wire_bytes = int(4 * (lists.sum() + words.sum()) + 16 * P)
-    # rounds over peer distance t: sends to rank + t, receives from rank - t;
-    # a round closes once the largest receive volume (over ranks) would pass
-    # round_words -- the grouping must be the same on every rank
-    vol = torch.zeros(P, dtype=torch.int64, device=dev)
-    for t in range(1, P):
-        if rank - t >= 0:
-            vol[t] = int(rwords[rank - t])
-    vol = yield ("allreduce", vol, "max")
-    vol = vol.cpu().numpy()
-    rounds, cur, acc = [], [], 0
-    for t in range(1, P):
-        w = int(vol[t])
-        if cur and acc + w > round_words:
-            rounds.append(cur)
-            cur, acc = [], 0
-        cur.append(t)
-        acc += w
-    if cur:
-        rounds.append(cur)
     pending = None
     for rd in rounds:
         sl, sw = np.zeros(P, np.int64), np.zeros(P, np.int64)

@@ -224,9 +224,10 @@ class NumpyShardOps:
             np.add.at(acc, ix[ip[v]: ip[v + 1]], d - np.arange(d) - 1 + S.SEG_WEIGHT)
         return torch.as_tensor(acc)
 
-    def engine_cost(self, acc, effdeg, n, tab_weight=1):
+    def engine_cost(self, acc, effdeg, n, tab_weight=1, send_weight=0):
         a, d = self._np(acc), self._np(effdeg).astype(np.int64)
-        return torch.as_tensor(np.where((d > 0) & (a > 0), a + tab_weight * d + 16, 0).astype(np.int64))
+        return torch.as_tensor((np.where((d > 0) & (a > 0), a + tab_weight * d + 16, 0) + send_weight * d)
+                               .astype(np.int64))
 
     # -- count --
     def _rows(self, sh):
