@@ -444,6 +444,36 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
                    const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr, int32_t* rev_seg,
                    int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream);
 
+/* ------------------------------------------------------------ NCCL layer */
+
+/* The collectives of the multi-GPU schemes for a caller that binds this
+ * library directly: communicator setup, the
+ * all-reduce of the per-rank partials (reduce_sum, runtime.py:255-259) and
+ * the list exchange of the surrogate scheme (space_efficient.py:116-144) as
+ * grouped ncclSend/ncclRecv.  libnccl is loaded at the first call (dlopen of
+ * $TCB_NCCL_LIB, else libnccl.so.2); every call is stream-ordered. */
+typedef struct tc_nccl_s* tc_nccl_t;
+enum { TC_DT_U8 = 0, TC_DT_I32 = 1, TC_DT_I64 = 2, TC_DT_U64 = 3 };
+enum { TC_OP_SUM = 0, TC_OP_MAX = 1, TC_OP_MIN = 2 };
+/* 128-byte unique id for tc_nccl_init_rank (rank 0 creates, all share). */
+int tc_nccl_unique_id(void* id_out);
+int tc_nccl_init_rank(const void* id, int32_t nranks, int32_t rank, tc_nccl_t* comm);
+/* One process driving ndev GPUs (ncclCommInitAll). */
+int tc_nccl_init_all(int32_t ndev, const int32_t* devices, tc_nccl_t* comms);
+int tc_nccl_free(tc_nccl_t comm);
+/* In-place all-reduce of count elements (TC_DT_*, TC_OP_*). */
+int tc_allreduce(void* buf, int64_t count, int32_t dtype, int32_t op, tc_nccl_t comm, tc_stream_t stream);
+/* In-place SUM of uint64 counts (the per-rank triangle partials). */
+int tc_allreduce_u64(unsigned long long* buf, int64_t count, tc_nccl_t comm, tc_stream_t stream);
+/* All-to-all-v: send_counts[p] elements to rank p from consecutive send
+ * offsets, recv_counts[p] from rank p into consecutive recv offsets (host
+ * count arrays of nranks entries). */
+int tc_exchange(const void* send, const int64_t* send_counts, void* recv, const int64_t* recv_counts, int32_t dtype,
+                int32_t nranks, tc_nccl_t comm, tc_stream_t stream);
+/* tc_exchange of int32 list ids (the surrogate's packed N^_v lists). */
+int tc_exchange_lists(const int32_t* send, const int64_t* send_counts, int32_t* recv, const int64_t* recv_counts,
+                      int32_t nranks, tc_nccl_t comm, tc_stream_t stream);
+
 /* ------------------------------------------------------------ generators */
 
 /* ER G(n,m) raw pairs (configs 1, 5): out int32[2m]. */

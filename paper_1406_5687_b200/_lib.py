@@ -73,6 +73,14 @@ _SIGS = {
     "tc_shard_send_sizes": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
     "tc_shard_send_pack": [_vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
+    "tc_nccl_unique_id": [_vp],
+    "tc_nccl_init_rank": [_vp, _i32, _i32, ctypes.POINTER(_vp)],
+    "tc_nccl_init_all": [_i32, _vp, _vp],
+    "tc_nccl_free": [_vp],
+    "tc_allreduce": [_vp, _i64, _i32, _i32, _vp, _vp],
+    "tc_allreduce_u64": [_vp, _i64, _vp, _vp],
+    "tc_exchange": [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp],
+    "tc_exchange_lists": [_vp, _vp, _vp, _vp, _i32, _vp, _vp],
     "tc_parse_edge_list": [_vp, _i64, _vp, _i64, _pi64, _pi64, _pi64, ctypes.POINTER(ctypes.c_int32),
                            ctypes.POINTER(ctypes.c_int32), _vp],
     "tc_gen_er": [_i64, _i64, _u64, _vp, _vp],
@@ -91,10 +99,26 @@ def build_library(force=False):
     return _SO
 
 
+def _nccl_path():
+    """The NCCL the C ABI's collectives dlopen (torch's pip NCCL), unless
+    TCB_NCCL_LIB says otherwise."""
+    if os.environ.get("TCB_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as nn
+
+        p = os.path.join(list(nn.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ["TCB_NCCL_LIB"] = p
+    except ImportError:
+        pass
+
+
 def lib():
     """Load the library (build it first if absent)."""
     global _LIB
     if _LIB is None:
+        _nccl_path()
         if not os.path.exists(_SO):
             build_library()
         L = ctypes.CDLL(_SO)

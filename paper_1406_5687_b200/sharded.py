@@ -367,6 +367,80 @@ def ops_of(gen):
         return None
 
 
+class CComm:
+    """A communicator of the C ABI's NCCL layer (tc_nccl_*, tc_allreduce,
+    tc_exchange): the path a reference-side binding drives without
+    torch.distributed."""
+
+    DT = {torch.uint8: 0, torch.int32: 1, torch.int64: 2}
+    OP = {"sum": 0, "max": 1, "min": 2}
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        from . import _lib
+
+        self.L, self.P, self.rank = _lib, nranks, rank
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(uid, 128)
+        _lib.call("tc_nccl_init_rank", buf, int(nranks), int(rank), ctypes.byref(h))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        from . import _lib
+
+        buf = ctypes.create_string_buffer(128)
+        _lib.call("tc_nccl_unique_id", buf)
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            self.L.lib().tc_nccl_free(self.h)
+            self.h = None
+
+    def allreduce(self, t, op):
+        self.L.call("tc_allreduce", self.L.ptr(t), int(t.numel()), self.DT[t.dtype], self.OP[op], self.h,
+                    self.L.stream())
+        return t
+
+    def exchange(self, send, counts, rcounts, recv=None):
+        """all-to-all-v along dim 0 (counts in rows)."""
+        row = int(np.prod(send.shape[1:])) if send.dim() > 1 else 1
+        if recv is None:
+            recv = torch.empty((int(np.sum(rcounts)),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        sc = (np.asarray(counts, np.int64) * row).astype(np.int64)
+        rc = (np.asarray(rcounts, np.int64) * row).astype(np.int64)
+        self.L.call("tc_exchange", self.L.ptr(send.contiguous()), sc.ctypes.data_as(ctypes.c_void_p),
+                    self.L.ptr(recv), rc.ctypes.data_as(ctypes.c_void_p), self.DT[send.dtype], self.P, self.h,
+                    self.L.stream())
+        return recv
+
+
+def run_capi(gen, comm: CComm):
+    """Drives one rank's generator over the C ABI's NCCL layer."""
+    res = None
+    while True:
+        try:
+            req = gen.send(res)
+        except StopIteration as stop:
+            return stop.value
+        kind = req[0]
+        if kind == "allreduce":
+            res = comm.allreduce(req[1], req[2])
+        elif kind == "a2a":
+            send, counts = req[1], np.asarray(req[2], np.int64)
+            ct = torch.as_tensor(counts).to(send.device)
+            rc = comm.exchange(ct, np.ones(comm.P, np.int64), np.ones(comm.P, np.int64))
+            rcounts = rc.cpu().numpy()
+            res = (comm.exchange(send, counts, rcounts), rcounts)
+        elif kind == "a2a_start":  # stream-ordered: the wait is a no-op for the host
+            into = req[4] if len(req) > 4 else None
+            res = comm.exchange(req[1], req[2], req[3], into)
+        elif kind == "wait":
+            res = req[1]
+        else:
+            raise ValueError(f"unknown collective {kind}")
+
+
 def emulate(gens, timed=False):
     """Runs P rank generators in lockstep in this process (one device): every
     collective is performed once all ranks have reached it.  With timed=True

@@ -85,3 +85,37 @@ def test_bench_multi_gpu_path_world1(mode, tmp_path):
         part = line["partitioned"][0]
         assert part.get("error") is None, part
         assert part["triangles"] == 722 and part["triangles_ok"] and part["n_gpus"] == 1
+
+
+def test_capi_nccl_layer_world1():
+    """The C ABI's own NCCL layer (tc_nccl_*, tc_allreduce_u64,
+    tc_exchange_lists) at world size 1, and the sharded pipeline driven
+    through it without torch.distributed."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_1406_5687_b200 import _lib
+    from paper_1406_5687_b200 import sharded as S
+
+    torch.cuda.set_device(0)
+    comm = S.CComm(S.CComm.unique_id(), 1, 0)
+    try:
+        x = torch.arange(5, dtype=torch.int64, device="cuda")
+        _lib.call("tc_allreduce_u64", _lib.ptr(x), 5, comm.h, _lib.stream())
+        assert x.tolist() == [0, 1, 2, 3, 4]
+        src = torch.arange(10, dtype=torch.int32, device="cuda")
+        dst = torch.zeros(10, dtype=torch.int32, device="cuda")
+        n = np.array([10], np.int64)
+        _lib.call("tc_exchange_lists", _lib.ptr(src), n.ctypes.data_as(ctypes.c_void_p), _lib.ptr(dst),
+                  n.ctypes.data_as(ctypes.c_void_p), 1, comm.h, _lib.stream())
+        assert torch.equal(src, dst)
+        raw = rmat_edges(13, 16, 7)
+        g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw)))
+        T = tcb.count_triangles_seq(g)
+        sh = S.run_capi(S.build_gen(raw.contiguous(), 0, 1, 0, "engine"), comm)
+        assert torch.equal(sh.indices, g.eff_indices)
+        total, met = S.run_capi(S.count_gen(sh, 1, 0, round_words=4096), comm)
+        assert total == T and met.triangles == T
+    finally:
+        comm.close()
