@@ -49,7 +49,16 @@ int tc_abi_version(void);
 /* Number of this library's kernels launched so far in the process (CUB's
  * sort/scan kernels excluded).  Measurement only. */
 unsigned long long tc_launch_count(void);
-/* Releases pooled scratch back to the driver (between large jobs). */
+/* Device memory.  Every scratch / plan allocation of the library goes to the
+ * caller's allocator when one is registered (e.g. torch's caching allocator,
+ * so the caller owns every byte; register before the first call), else to a
+ * stream-ordered pool private to the library (the device's default pool is
+ * never modified).  alloc returns NULL on failure (-> TC_ENOMEM); frees are
+ * stream-ordered on the given stream.  NULL, NULL restores the pool. */
+typedef void* (*tc_alloc_fn)(size_t bytes, tc_stream_t stream, void* ctx);
+typedef void (*tc_free_fn)(void* ptr, tc_stream_t stream, void* ctx);
+int tc_set_allocator(tc_alloc_fn alloc, tc_free_fn free_fn, void* ctx);
+/* Releases the private pool's cached blocks back to the driver. */
 int tc_trim_pool(void);
 
 /* ---------------------------------------------------------------- build */

@@ -25,6 +25,7 @@ _pi64 = ctypes.POINTER(ctypes.c_int64)
 _SIGS = {
     "tc_abi_version": [],
     "tc_trim_pool": [],
+    "tc_set_allocator": [_vp, _vp, _vp],
     "tc_normalize": [_vp, _i64, _vp, _pi64, _pi64, _vp],
     "tc_build_graph": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "tc_build_graph_deg": [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -165,3 +166,30 @@ def ptr(t):
     if t is None:
         return None
     return ctypes.c_void_p(t.data_ptr())
+
+
+_ALLOC_CB = []  # every registered callback pair stays alive: blocks are freed by the allocator that made them
+
+
+def use_torch_allocator(enable=True):
+    """Route the library's scratch and plan memory through torch's caching
+    allocator (tc_set_allocator), so torch owns every device byte."""
+    L = lib()
+    if not enable:
+        check(L.tc_set_allocator(None, None, None))
+        return
+    AF = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+    FF = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+    def _alloc(nbytes, stream, _ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0))
+        except Exception:  # noqa: BLE001 -- reported to the library as NULL (TC_ENOMEM)
+            return None
+
+    def _free(ptr, _stream, _ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    cb = (AF(_alloc), FF(_free))
+    _ALLOC_CB.append(cb)
+    check(L.tc_set_allocator(ctypes.cast(cb[0], ctypes.c_void_p), ctypes.cast(cb[1], ctypes.c_void_p), None))

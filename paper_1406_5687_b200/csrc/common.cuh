@@ -50,31 +50,34 @@ int guarded(F&& body) {
   }
 }
 
-// Stream-ordered scratch memory (cudaMallocAsync from the device pool);
-// everything is released on the same stream when the guard dies, so the
-// library never holds device memory across calls.
+// Library device memory (abi.cu): the caller's allocator if registered
+// (tc_set_allocator), else the library's private stream-ordered pool.
+struct DevBlock {
+  void* p;
+  tc_free_fn free_fn;  // NULL: the library pool
+  void* ctx;
+};
+DevBlock dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(const DevBlock& b, cudaStream_t s);
+
+// Stream-ordered scratch memory; everything is released on the same stream
+// when the guard dies, so the library never holds device memory across calls.
 class Scratch {
  public:
   explicit Scratch(cudaStream_t s) : s_(s) {}
   ~Scratch() {
-    for (void* p : ptrs_) cudaFreeAsync(p, s_);
+    for (const DevBlock& b : ptrs_) dev_free(b, s_);
   }
   template <class T>
   T* alloc(size_t n) {
-    void* p = nullptr;
-    size_t bytes = (n ? n : 1) * sizeof(T);
-    cudaError_t e = cudaMallocAsync(&p, bytes, s_);
-    if (e != cudaSuccess)
-      throw Error(TC_ENOMEM, std::string("cudaMallocAsync(") + std::to_string(bytes) +
-                                 "): " + cudaGetErrorString(e));
-    ptrs_.push_back(p);
-    return static_cast<T*>(p);
+    ptrs_.push_back(dev_alloc((n ? n : 1) * sizeof(T), s_));
+    return static_cast<T*>(ptrs_.back().p);
   }
   void* bytes(size_t n) { return alloc<unsigned char>(n); }
 
  private:
   cudaStream_t s_;
-  std::vector<void*> ptrs_;
+  std::vector<DevBlock> ptrs_;
 };
 
 inline int bits_for(uint64_t v) {

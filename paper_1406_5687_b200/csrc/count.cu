@@ -1571,14 +1571,14 @@ class Persist {
   ~Persist() { release(); }
   void set_stream(cudaStream_t s) { s_ = s; }
   void release() {
-    for (void* p : ptrs_) cudaFreeAsync(p, 0);
+    // on the legacy default stream (ordered after work on blocking streams,
+    // e.g. runs of the plan issued elsewhere)
+    for (const DevBlock& b : ptrs_) dev_free(b, 0);
     ptrs_.clear();
   }
   void* bytes(size_t n) {  // pool allocation, valid on every stream once s_ has synchronised
-    void* p = nullptr;
-    TC_CUDA(cudaMallocAsync(&p, n ? n : 16, s_));
-    ptrs_.push_back(p);
-    return p;
+    ptrs_.push_back(dev_alloc(n ? n : 16, s_));
+    return ptrs_.back().p;
   }
   template <class T>
   T* alloc(int64_t n) {
@@ -1586,7 +1586,7 @@ class Persist {
   }
 
  private:
-  std::vector<void*> ptrs_;
+  std::vector<DevBlock> ptrs_;
   cudaStream_t s_ = 0;
 };
 
