@@ -345,6 +345,9 @@ __global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int3
       if (u < u0 || u >= u1) continue;
       const int64_t slot = (e + 1 < wend) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
                                           : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
+#if TCB_DEBUG
+      assert(slot >= rev_indptr[u] && slot < rev_indptr[u + 1]);
+#endif
       // the suffix of N^_w after u, in pool coordinates
       rev_seg[slot] = make_int2((int)(p0 + (e + 1 - wbeg)), (int)(p0 + (wend - wbeg)));
     }

@@ -4,6 +4,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cassert>
+
+// TCB_DEBUG=1 builds device-side bounds asserts into the engine and the
+// scatter kernels (tools/build_variant.sh debug -DTCB_DEBUG=1; the GPU pool
+// has no compute-sanitizer).
+#ifndef TCB_DEBUG
+#define TCB_DEBUG 0
+#endif
+
 #include <stdexcept>
 #include <string>
 #include <vector>

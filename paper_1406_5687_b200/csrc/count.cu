@@ -370,6 +370,9 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
       }
       const int f = b + lane;
       if (f < total) {
+#if TCB_DEBUG
+        assert(sj >= 0 && sj < 32 && f >= segtab[sj].z && f <= (segtab[sj].w >> 8));
+#endif
 #if TCB_SEGPTR
         const int4 q = segtab[sj];  // (&pool4[delta] lo, hi, excl, (endx - 1) << 8 | last mask << 4 | first mask)
         const int4* p = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
@@ -929,6 +932,14 @@ __device__ __forceinline__ void small_window(const int4* __restrict__ pool4, con
     sj = __popc(before) - 1 + __popc(starts & ((2u << lane) - 1u));
   }
   const int f = b + lane;
+#if TCB_DEBUG
+  {  // the resolved segment covers chunk f (the tail segment: f >= total)
+    assert(sj >= 0 && sj <= 32);
+    const int last = segtab[sj].y >> 8, prev = sj ? (segtab[sj - 1].y >> 8) : -1;
+    assert(f > prev && (f <= last || f >= total));
+    if (kPadded && f >= total) assert(segtab[sj].x + f >= -32 && segtab[sj].x + f < 0);
+  }
+#endif
   if (kPadded) {
     // chunks past `total` resolve to the tail segment (INT32_MAX head of the
     // pool); ids before a suffix's start in its first chunk are <= u and ids
@@ -1045,7 +1056,7 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
   }
   if (kPadded && lane == 0) {
     // tail segment: chunk f >= total reads pool4[f - total - 32], in the head
-    segtab[nseg] = make_int2(-total - 32, 0);
+    segtab[nseg] = make_int2(-total - 32, 0x7FFFFF << 8);
     if (fast) atomicOr(&sbits[total >> 5], 1u << (total & 31));
   }
   __syncwarp();

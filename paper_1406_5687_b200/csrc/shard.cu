@@ -124,11 +124,18 @@ __global__ void k_sh_keys(const int2* __restrict__ pairs, int64_t m, const int32
 // scatter into groups by destination (order inside a group unspecified)
 template <class T>
 __global__ void k_sh_group(const T* __restrict__ in, const int32_t* __restrict__ dest, int64_t m,
-                           const long long* __restrict__ off, long long* cursor, T* out) {
+                           const long long* __restrict__ counts, const long long* __restrict__ off, long long* cursor,
+                           T* out) {
   GRID_STRIDE(i, m) {
     const int d = dest[i];
     if (d < 0) continue;
-    out[off[d] + add64(&cursor[d], 1ll)] = in[i];
+    const long long c = add64(&cursor[d], 1ll);
+#if TCB_DEBUG
+    assert(c < counts[d]);
+#else
+    (void)counts;
+#endif
+    out[off[d] + c] = in[i];
   }
 }
 
@@ -415,7 +422,11 @@ __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* _
       const int32_t u = pool[p + i];
       if (u >= lo && u < hi) {
         const int64_t x = u - lo;
-        rev_seg[rev_indptr[x] + atomicAdd(&cursor[x], 1)] = make_int2((int)(p + i + 1), (int)(p + d));
+        const int64_t slot = rev_indptr[x] + atomicAdd(&cursor[x], 1);
+#if TCB_DEBUG
+        assert(slot < rev_indptr[x + 1]);
+#endif
+        rev_seg[slot] = make_int2((int)(p + i + 1), (int)(p + d));
       }
     }
   }
@@ -518,7 +529,7 @@ int tc_shard_keys(const int32_t* pairs, int64_t m, const int32_t* map, int32_t P
     k_sh_keys<<<grid_for(m, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(pairs), m, map, P, key, dest, cnt);
     check_launch();
     ex_sum(sc, cnt, cnt + P, P, s);
-    k_sh_group<<<grid_for(m, kBlk), kBlk, 0, s>>>(key, dest, m, cnt + P, cnt + 2 * P,
+    k_sh_group<<<grid_for(m, kBlk), kBlk, 0, s>>>(key, dest, m, cnt, cnt + P, cnt + 2 * P,
                                                  reinterpret_cast<unsigned long long*>(keys_out));
     check_launch();
     TC_CUDA(cudaMemcpyAsync(counts_host, cnt, P * sizeof(long long), cudaMemcpyDeviceToHost, s));
@@ -630,7 +641,7 @@ int tc_shard_route(const int32_t* lohi, int64_t k, const int64_t* bounds, int32_
     k_sh_route_dest<<<grid_for(k, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(lohi), k, bounds, P, dest, cnt);
     check_launch();
     ex_sum(sc, cnt, cnt + P, P, s);
-    k_sh_group<<<grid_for(k, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(lohi), dest, k, cnt + P, cnt + 2 * P,
+    k_sh_group<<<grid_for(k, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(lohi), dest, k, cnt, cnt + P, cnt + 2 * P,
                                                  reinterpret_cast<int2*>(out));
     check_launch();
     TC_CUDA(cudaMemcpyAsync(counts_host, cnt, P * sizeof(long long), cudaMemcpyDeviceToHost, s));

@@ -1,10 +1,13 @@
 """Small workload for compute-sanitizer: every engine tier (forced caps), both
-formulations, partitioning, surrogate, parser, generators (dev/CI tool)."""
+formulations, the padded-pool and list-pool streaming paths, partitioning,
+surrogate, the sharded multi-rank pipeline (emulated), the host-input
+normalize pipeline, parser, generators (dev/CI tool)."""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+os.environ.setdefault("TCB_HOST_PIPELINE_MIN", "4096")  # small lists take the chunked host pipeline too
 import torch  # noqa: E402
 
 import paper_1406_5687_b200 as tcb  # noqa: E402
@@ -36,5 +39,15 @@ for g in graphs:
     tcb.count_dynamic(g, 5)
     _ = g.full_indices
 tcb.load_edge_list(b"# x\n0 1\n1 2\n2 0\n")
+# host-input normalize (chunked copy + merges) and the sharded pipeline
+from paper_1406_5687_b200 import sharded as S  # noqa: E402
+raw = rmat_edges(12, 8, 4)
+host = torch.empty(tuple(raw.shape), dtype=torch.int32, pin_memory=True)
+host.copy_(raw)
+gh = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=host)))
+T = tcb.count_triangles_seq(gh)
+for cost in ("predsum", "engine"):
+    shards, _ = S.emulate_build(raw, 3, cost=cost)
+    assert S.emulate_count(shards, round_words=256)[0] == T
 torch.cuda.synchronize()
 print("sanitize workload ok")
