@@ -41,6 +41,7 @@
 // shrinking tasks of (remaining / workers); workers pull chunk indices from
 // one global atomic counter (the coordinator's queue).
 #include <cub/cub.cuh>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -862,6 +863,9 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
 #ifndef TCB_SMALL_V20
 #define TCB_SMALL_V20 1
 #endif
+#ifndef TCB_SBITS_MATCH
+#define TCB_SBITS_MATCH 0  // 1: match_any + reduce_or (measured: spills, cfg2 1.70 -> 1.98 ms)
+#endif
 #ifndef TCB_SMALL_W
 #define TCB_SMALL_W 3  // windows per step
 #endif
@@ -1048,12 +1052,23 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
   const bool fast = kPadded ? total < 32 * kSmallSbW : total <= 32 * kSmallSbW;
   const bool lane_seg = lane < nseg;
   __syncwarp();  // the previous group's reads of segtab / sbits are done
-  if (lane_seg) {
+  if (lane_seg)
     // chunk f of this segment is pool4[c0s - excl + f]; last chunk incl - 1 (< 2^23:
     // oriented lists hold at most sqrt(2m) ids)
     segtab[lane] = make_int2(c0s - excl, ((incl - 1) << 8) | (lm << 4) | fm);
-    if (fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
+#if TCB_SBITS_MATCH
+  if (fast) {
+    // starts are distinct and ascending: the lanes sharing a bitmap word OR
+    // their bits with one reduction and its lowest lane stores the word (no
+    // shared atomics on the same word)
+    const unsigned w = lane_seg ? (unsigned)(excl >> 5) : 0xFFFFFFFFu;
+    const unsigned grp = __match_any_sync(FULL, w);
+    const unsigned bits = __reduce_or_sync(grp, lane_seg ? 1u << (excl & 31) : 0u);
+    if (lane_seg && lane == __ffs(grp) - 1) sbits[w] = bits;
   }
+#else
+  if (lane_seg && fast) atomicOr(&sbits[excl >> 5], 1u << (excl & 31));  // starts are distinct (nch >= 1)
+#endif
   if (kPadded && lane == 0) {
     // tail segment: chunk f >= total reads pool4[f - total - 32], in the head
     segtab[nseg] = make_int2(-total - 32, 0x7FFFFF << 8);
@@ -1689,6 +1704,97 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
   return L;
 }
 
+// Concurrent tier launches (one stream per tier, the block tier first):
+// measured cfg 4 -0.8 %, cfg 5 +5.8 % (the first kernel holds every SM until
+// its tail, and the small tier's blocks then compete with the mid tier's) --
+// off by default.
+#ifndef TCB_TIER_STREAMS
+#define TCB_TIER_STREAMS 0
+#endif
+
+template <class Segs>
+static void launch_tier(EngineLaunch& L, int k, Segs segs, cudaStream_t s, const TierShape& ts) {
+  if (k == 0) {
+#if TCB_SMALL_V20
+    if (L.args[0].padded) k_small<Segs, true><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    else k_small<Segs, false><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+#else
+    K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+#endif
+  } else if (k == 1) {
+    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
+  } else {
+    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
+  }
+  check_launch();
+}
+
+struct TierStreams {
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t t0[3] = {nullptr, nullptr, nullptr}, t1[3] = {nullptr, nullptr, nullptr};
+  std::mutex mu;
+};
+
+static TierStreams& tier_streams() {
+  static TierStreams ts[64];
+  int dev = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  TierStreams& t = ts[dev];
+  if (!t.fork) {
+    std::lock_guard<std::mutex> lk(t.mu);
+    if (!t.fork) {
+      for (int k = 0; k < 3; ++k) {
+        TC_CUDA(cudaStreamCreateWithFlags(&t.st[k], cudaStreamNonBlocking));
+        TC_CUDA(cudaEventCreateWithFlags(&t.join[k], cudaEventDisableTiming));
+        TC_CUDA(cudaEventCreate(&t.t0[k]));
+        TC_CUDA(cudaEventCreate(&t.t1[k]));
+      }
+      cudaEvent_t f;
+      TC_CUDA(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
+      t.fork = f;
+    }
+  }
+  return t;
+}
+
+template <class Segs>
+static void launch_tiers_concurrent(EngineLaunch& L, Segs segs, cudaStream_t s, const TierShape& ts) {
+  TierStreams& T = tier_streams();
+  std::lock_guard<std::mutex> lk(T.mu);  // the fork/join events are shared per device
+  if (g_time_engine) {
+    if (!g_ev[0]) {
+      TC_CUDA(cudaEventCreate(&g_ev[0]));
+      TC_CUDA(cudaEventCreate(&g_ev[1]));
+    }
+    TC_CUDA(cudaEventRecord(g_ev[0], s));
+  }
+  TC_CUDA(cudaEventRecord(T.fork, s));  // after the queue resets and the caller's prior work
+  for (int k = 2; k >= 0; --k) {
+    if (!L.hsz[k]) continue;
+    TC_CUDA(cudaStreamWaitEvent(T.st[k], T.fork, 0));
+    if (g_time_engine) TC_CUDA(cudaEventRecord(T.t0[k], T.st[k]));
+    launch_tier<Segs>(L, k, segs, T.st[k], ts);
+    if (g_time_engine) TC_CUDA(cudaEventRecord(T.t1[k], T.st[k]));
+    TC_CUDA(cudaEventRecord(T.join[k], T.st[k]));
+  }
+  for (int k = 0; k < 3; ++k)
+    if (L.hsz[k]) TC_CUDA(cudaStreamWaitEvent(s, T.join[k], 0));
+  if (g_time_engine) {
+    TC_CUDA(cudaEventRecord(g_ev[1], s));
+    TC_CUDA(cudaEventSynchronize(g_ev[1]));
+    float ms = 0.f;
+    TC_CUDA(cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]));
+    g_engine_ms += ms;
+    for (int k = 0; k < 3; ++k)
+      if (L.hsz[k]) {
+        TC_CUDA(cudaEventElapsedTime(&ms, T.t0[k], T.t1[k]));
+        g_tier_ms[k] += ms;
+      }
+    ++g_engine_launches;
+  }
+}
+
 // Launches the non-empty tiers (queue counters reset first); `out` must be
 // zeroed by the caller.
 template <class Segs>
@@ -1701,6 +1807,16 @@ void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStre
     L.args[k].stride = stride;
     if (L.hsz[k]) TC_CUDA(cudaMemsetAsync(L.queue[k], 0, sizeof(int), s));
   }
+  int nonempty = (L.hsz[0] > 0) + (L.hsz[1] > 0) + (L.hsz[2] > 0);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  TC_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (TCB_TIER_STREAMS && nonempty > 1 && cap == cudaStreamCaptureStatusNone) {
+    // Concurrent tiers: each tier on its own stream, the longest (block)
+    // first, so a tier's tail overlaps the next tier's work instead of
+    // idling the SMs that finished early.
+    launch_tiers_concurrent(L, segs, s, ts);
+    return;
+  }
   if (g_time_engine) {
     if (!g_ev[0]) {
       TC_CUDA(cudaEventCreate(&g_ev[0]));
@@ -1712,23 +1828,15 @@ void launch_engine(EngineLaunch& L, unsigned long long* out, Segs segs, cudaStre
     TC_CUDA(cudaEventRecord(g_tev[0], s));
   }
   if (L.hsz[0]) {
-#if TCB_SMALL_V20
-    if (L.args[0].padded) k_small<Segs, true><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
-    else k_small<Segs, false><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
-#else
-    K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
-#endif
-    check_launch();
+    launch_tier<Segs>(L, 0, segs, s, ts);
   }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[1], s));
   if (L.hsz[1]) {
-    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
-    check_launch();
+    launch_tier<Segs>(L, 1, segs, s, ts);
   }
   if (g_time_engine) TC_CUDA(cudaEventRecord(g_tev[2], s));
   if (L.hsz[2]) {
-    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
-    check_launch();
+    launch_tier<Segs>(L, 2, segs, s, ts);
   }
   if (g_time_engine) {
     TC_CUDA(cudaEventRecord(g_tev[3], s));

@@ -687,3 +687,30 @@ def test_replicated_parts_sum_to_total(parts):
         assert min(got) > 0, got
     with pytest.raises(ValueError):
         count_middle_part(g, parts, parts)
+
+
+def test_intersect_count_randomized():
+    """intersect_count (sequential.py:20-27) on seeded random ascending lists
+    of mixed lengths and overlaps against the oracle's merge_count
+    (_kernels.py:15-37), including empty, disjoint, identical, nested and
+    skewed (1 vs 10^5) pairs -- the reference models it with a hash-set
+    oracle (test_sequential.py:21-28)."""
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(20261021)
+    cases = [([], []), ([], [1, 2]), ([5], [5]), ([1, 2, 3], [4, 5, 6]), (list(range(100)), list(range(100)))]
+    for _ in range(60):
+        na, nb = (int(x) for x in rng.integers(0, 3000, 2))
+        span = int(rng.choice([50, 5000, 2**31 - 2]))
+        a = np.unique(rng.integers(0, span, na))
+        b = np.unique(rng.integers(0, span, nb))
+        cases.append((a, b))
+    big = np.unique(rng.integers(0, 10**7, 100_000))
+    cases += [(big[:1], big), (big[::7], big[3::5]), (big, big[::2])]
+    for a, b in cases:
+        a = np.asarray(a, np.int64)
+        b = np.asarray(b, np.int64)
+        want = O.intersect_size(a, b)
+        assert want == len(set(a.tolist()) & set(b.tolist()))
+        assert tcb.intersect_count(a, b) == want
+        assert tcb.intersect_count(b, a) == want
