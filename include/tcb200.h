@@ -431,9 +431,13 @@ int tc_shard_engine_cost_fin(const uint64_t* acc, const int32_t* effdeg, int64_t
 /* Surrogate send plan (_kernels.py:94-126 LastProc records, one message per
  * (v, dest > rank) with an id of N^_v owned by dest; the message is row v of
  * the shard's padded pool from the 16-byte chunk holding its first id >=
- * bounds[dest] on): sizes_dev int64[3P] = lists, padded words, whole-list
- * words per destination (the last is the reference's bytes_sent
- * accounting); copied to sizes_host if not NULL (synchronises).  P <= 32. */
+ * bounds[dest] on): sizes_dev int64[tc_shard_send_plan_len] = lists, padded
+ * words, whole-list words per destination (3P entries; the last is the
+ * reference's bytes_sent accounting; copied to sizes_host if not NULL, which
+ * synchronises), followed by the pack kernel's per-block first list / word
+ * slots (static for a partitioned graph: the pack then runs without a
+ * counting pass and without global atomics).  P <= 32. */
+int tc_shard_send_plan_len(int64_t nrow, int32_t P, int64_t* len_host);
 int tc_shard_send_sizes(const int64_t* indptr, const int32_t* indices, int64_t nrow, const int64_t* pool_indptr,
                         const int64_t* bounds, int32_t P, int32_t rank, int64_t* sizes_dev, int64_t* sizes_host,
                         tc_stream_t stream);

@@ -71,6 +71,7 @@ _SIGS = {
     "tc_shard_pool": [_vp, _vp, _i64, _vp, _vp, _vp],
     "tc_shard_engine_cost": [_vp, _vp, _i64, _i64, _vp, _vp],
     "tc_shard_engine_cost_fin": [_vp, _vp, _i64, _i64, _i64, _vp, _vp],
+    "tc_shard_send_plan_len": [_i64, _i32, _pi64],
     "tc_shard_send_sizes": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
     "tc_shard_send_pack": [_vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],

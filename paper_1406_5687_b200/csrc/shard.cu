@@ -272,102 +272,205 @@ __device__ __forceinline__ int64_t row_lb(const int32_t* __restrict__ ids, int64
 // row of the padded pool from the 16-byte chunk holding the first id >=
 // bounds[j] to the row's padded end (the few leading ids of that chunk are
 // < bounds[j]: they never own a segment and never lie in a suffix).
-// Per destination: lists, padded ids, whole-list words (the reference's
-// bytes_sent accounting).  Lane = destination.
-__global__ void k_sh_send_count(const int64_t* __restrict__ indptr, const int32_t* __restrict__ ids, int64_t nrow,
-                                const int64_t* __restrict__ pptr, const int64_t* __restrict__ bounds, int P,
-                                int rank, long long* lists, long long* words, long long* full) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+//
+// Work layout of both send kernels: a warp handles 32 / G rows at a time
+// (steps interleaved over all the grid's warps), G = max(8, pow2 >= P - 1 - rank)
+// lanes per row, lane jl of a row's group standing for destination
+// rank + 1 + jl; the rows of a warp and their order are fixed by (block,
+// warp, nrow) alone.  The count kernel leaves, per (warp, destination), the
+// warp's lists and padded words; a prefix over the warps turns them into
+// each warp's first list / word slot inside each destination's part of the
+// send buffers (the "send plan": static for a partitioned graph, kept with
+// the sizes).  The pack kernel then needs no atomics and no counting pass,
+// and its output is deterministic: a warp walks its rows with running
+// offsets per destination (a prefix over the row slots of each step by
+// shuffles) and the group's lanes copy each message as 16-byte chunks of
+// the padded pool.
+static constexpr int kEmitMaxP = 32;
+static constexpr int kSendWarps = kBlk / 32;
+
+static int send_group(int P, int rank) {  // lanes per row
+  int g = 8;
+  while (g < P - 1 - rank) g <<= 1;
+  return g;
+}
+
+static int send_blocks(int64_t nrow) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((nrow + 255) / 256, (int64_t)sm_count() * 8));
+}
+
+// first id >= bj of row [a, a + d); true when it is owned by the destination
+__device__ __forceinline__ bool send_msg(const int32_t* __restrict__ ids, int64_t a, int64_t d, int64_t bj,
+                                         int64_t bj1, int64_t& s) {
+  s = row_lb(ids, a, d, bj);
+  return s < d && ids[a + s] < bj1;
+}
+
+__global__ void __launch_bounds__(kBlk) k_sh_send_count(const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ ids, int64_t nrow,
+                                                        const int64_t* __restrict__ pptr,
+                                                        const int64_t* __restrict__ bounds, int P, int rank, int G,
+                                                        long long* tot, long long* unit_l, long long* unit_w) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rpw = 32 / G, g = lane / G, jl = lane % G, j = rank + 1 + jl;
+  const int64_t unit = (int64_t)blockIdx.x * kSendWarps + warp, nunit = (int64_t)gridDim.x * kSendWarps;
+  const bool dest = j < P;
+  const int64_t bj = dest ? bounds[j] : 0, bj1 = dest ? bounds[j + 1] : 0;
   long long cl = 0, cw = 0, cf = 0;
-  const int j = lane;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nrow; v += nw) {
-    const int64_t a = indptr[v], d = indptr[v + 1] - a;
-    if (j > rank && j < P && d > 0) {
-      const int64_t s = row_lb(ids, a, d, bounds[j]), e = row_lb(ids, a, d, bounds[j + 1]);
-      if (s < e) {
+  if (dest)
+    // warp step q covers rows [q rpw, (q + 1) rpw); a warp takes the steps
+    // q = unit (mod nunit): rows ascend in degree, so contiguous runs per
+    // block would leave the last blocks with most of the ids
+    for (int64_t v = unit * rpw + g; v < nrow; v += nunit * rpw) {
+      const int64_t a = indptr[v], d = indptr[v + 1] - a;
+      int64_t s;
+      if (d > 0 && send_msg(ids, a, d, bj, bj1, s)) {
         ++cl;
         cw += (pptr[v + 1] - pptr[v]) - (s & ~3ll);
         cf += d;
       }
     }
+  for (int o = G; o < 32; o <<= 1) {  // over the row slots of each destination
+    cl += __shfl_xor_sync(FULL, cl, o);
+    cw += __shfl_xor_sync(FULL, cw, o);
+    cf += __shfl_xor_sync(FULL, cf, o);
   }
-  if (j < P) {
-    add64(&lists[j], cl);
-    add64(&words[j], cw);
-    add64(&full[j], cf);
+  if (g == 0 && dest) {
+    unit_l[unit * P + j] = cl;
+    unit_w[unit * P + j] = cw;
+    if (cl) {
+      add64(&tot[j], cl);
+      add64(&tot[P + j], cw);
+      add64(&tot[2 * P + j], cf);
+    }
   }
 }
 
-// Emit pass.  A block takes a contiguous run of rows; its warps (one row at
-// a time, lanes = destinations) first total the block's messages per
-// destination in shared memory, one thread claims the block's ranges with
-// one global atomic per destination, and the warps then claim slots inside
-// them and copy each message as 16-byte chunks of the padded pool.  A slot
-// claim is one 64-bit atomic holding the message count (high 26 bits) and
-// its words (low 38), so the lengths and the lists agree in order (which is
-// otherwise unspecified; the receiver's count does not depend on it).
-static constexpr int kEmitMaxP = 32;
-__device__ __forceinline__ bool send_dest(const int32_t* __restrict__ ids, int64_t a, int64_t d,
-                                          const int64_t* __restrict__ bounds, int lane, int P, int rank, int64_t& s) {
-  s = 0;
-  if (lane <= rank || lane >= P) return false;
-  s = row_lb(ids, a, d, bounds[lane]);
-  return s < row_lb(ids, a, d, bounds[lane + 1]);
+// Per destination (one warp each): the warps' counts become their first
+// slots, offset by the destinations before it.
+__global__ void k_sh_send_prefix(const long long* __restrict__ tot, int P, int64_t nunit, long long* unit_l,
+                                 long long* unit_w) {
+  const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  if (j >= P) return;
+  long long run_l = 0, run_w = 0;
+  for (int i = 0; i < j; ++i) {
+    run_l += tot[i];
+    run_w += tot[P + i];
+  }
+  for (int64_t b0 = 0; b0 < nunit; b0 += 32) {
+    const int64_t b = b0 + lane;
+    const long long vl = b < nunit ? unit_l[b * P + j] : 0, vw = b < nunit ? unit_w[b * P + j] : 0;
+    long long il = vl, iw = vw;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long yl = __shfl_up_sync(0xffffffffu, il, o), yw = __shfl_up_sync(0xffffffffu, iw, o);
+      if (lane >= o) {
+        il += yl;
+        iw += yw;
+      }
+    }
+    if (b < nunit) {
+      unit_l[b * P + j] = run_l + il - vl;
+      unit_w[b * P + j] = run_w + iw - vw;
+    }
+    run_l += __shfl_sync(0xffffffffu, il, 31);
+    run_w += __shfl_sync(0xffffffffu, iw, 31);
+  }
 }
 
-__global__ void k_sh_send_emit(const int64_t* __restrict__ indptr, const int32_t* __restrict__ ids, int64_t nrow,
-                               const int64_t* __restrict__ pptr, const int4* __restrict__ pool4,
-                               const int64_t* __restrict__ bounds, int P, int rank,
-                               const long long* __restrict__ list_off, const long long* __restrict__ word_off,
-                               unsigned long long* cur, int32_t* out_len, int4* out4) {
-  __shared__ unsigned long long btot[kEmitMaxP], bcur[kEmitMaxP];
-  __shared__ long long bl[kEmitMaxP], bw[kEmitMaxP];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int64_t per = (nrow + gridDim.x - 1) / gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(nrow, r0 + per);
-  if (threadIdx.x < kEmitMaxP) {
-    btot[threadIdx.x] = 0;
-    bcur[threadIdx.x] = 0;
+// lower bound of x in a shared-memory row of d ascending ids
+__device__ __forceinline__ int smem_lb(const int32_t* ids, int d, int64_t x) {
+  int lo = 0, hi = d;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ids[mid] < x) lo = mid + 1;
+    else hi = mid;
   }
-  __syncthreads();
-  for (int64_t v = r0 + warp; v < r1; v += nwarp) {  // block totals
-    const int64_t a = indptr[v], d = indptr[v + 1] - a;
-    if (d == 0) continue;
-    int64_t s;
-    if (send_dest(ids, a, d, bounds, lane, P, rank, s)) {
-      const int64_t nch = ((pptr[v + 1] - pptr[v]) >> 2) - (s >> 2);
-      atomicAdd(&btot[lane], (1ull << 38) + (unsigned long long)(4 * nch));
+  return lo;
+}
+
+static constexpr int kStageChunks = 32;  // rows of <= 128 ids are staged in shared memory
+
+__global__ void __launch_bounds__(kBlk) k_sh_send_emit(const int64_t* __restrict__ indptr,
+                                                       const int32_t* __restrict__ ids, int64_t nrow,
+                                                       const int64_t* __restrict__ pptr,
+                                                       const int4* __restrict__ pool4,
+                                                       const int64_t* __restrict__ bounds, int P, int rank, int G,
+                                                       const long long* __restrict__ base_l,
+                                                       const long long* __restrict__ base_w, int32_t* out_len,
+                                                       int4* out4) {
+  // Rows of <= 32 chunks (almost all of them) are read once: the row's G
+  // lanes stage its padded chunks in shared memory with up to 32 / G
+  // independent 16-byte loads each, the destinations' lanes search the staged
+  // ids, and the messages are written from shared memory -- two dependent
+  // global round trips per step (offsets, row) instead of one per search
+  // step and per message.  Longer rows search and copy from global memory.
+  __shared__ int4 s_row[kSendWarps][4][kStageChunks];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rpw = 32 / G, g = lane / G, jl = lane % G, j = rank + 1 + jl, ndest = P - 1 - rank;
+  const bool dest = j < P;
+  const int64_t bj = dest ? bounds[j] : 0, bj1 = dest ? bounds[j + 1] : 0;
+  const int64_t unit = (int64_t)blockIdx.x * kSendWarps + warp, nunit = (int64_t)gridDim.x * kSendWarps;
+  long long run_l = dest ? base_l[unit * P + j] : 0;        // next list slot of destination j (this warp)
+  long long run_c = dest ? base_w[unit * P + j] >> 2 : 0;   // next 16-byte chunk slot
+  const int last = (rpw - 1) * G + jl;                       // the last row slot's lane for this destination
+  const int32_t* pool = reinterpret_cast<const int32_t*>(pool4);
+  int4* row = s_row[warp][g];  // rpw <= 4 rows per warp step
+  (void)ids;
+  for (int64_t vb = unit * rpw; vb < nrow; vb += nunit * rpw) {  // warp-uniform trip count (steps as in the count)
+    const int64_t v = vb + g;
+    int64_t d = 0, p = 0;
+    if (v < nrow) {
+      d = indptr[v + 1] - indptr[v];
+      p = pptr[v];
     }
-  }
-  __syncthreads();
-  if (threadIdx.x < P && btot[threadIdx.x]) {  // the block's ranges
-    const unsigned long long old = atomicAdd(&cur[threadIdx.x], btot[threadIdx.x]);
-    bl[threadIdx.x] = list_off[threadIdx.x] + (long long)(old >> 38);
-    bw[threadIdx.x] = word_off[threadIdx.x] + (long long)(old & ((1ull << 38) - 1));
-  }
-  __syncthreads();
-  for (int64_t v = r0 + warp; v < r1; v += nwarp) {
-    const int64_t a = indptr[v], d = indptr[v + 1] - a;
-    if (d == 0) continue;
-    int64_t s;
-    const bool hit = send_dest(ids, a, d, bounds, lane, P, rank, s);
-    unsigned todo = __ballot_sync(0xffffffffu, hit);
-    const int64_t p0 = pptr[v] >> 2, pd = (pptr[v + 1] - pptr[v]) >> 2;  // in chunks
-    long long li = 0, wi = 0;
-    if (hit) {  // lane j claims this row's slot in destination j's block range
-      const int64_t nch = pd - (s >> 2);
-      const unsigned long long old = atomicAdd(&bcur[lane], (1ull << 38) + (unsigned long long)(4 * nch));
-      li = bl[lane] + (long long)(old >> 38);
-      wi = bw[lane] + (long long)(old & ((1ull << 38) - 1));
-      out_len[li] = (int32_t)(d - 4 * (s >> 2));
+    const int pd = (int)((d + 3) >> 2);
+    const bool staged = pd <= kStageChunks;
+    __syncwarp();  // the previous step's reads of the staged rows are done
+    if (staged)
+      for (int c = jl; c < pd; c += G) row[c] = __ldg(&pool4[(p >> 2) + c]);
+    __syncwarp();
+    int s = 0, nch = 0;
+    if (dest && d > 0) {
+      bool hit;
+      if (staged) {
+        const int32_t* rid = reinterpret_cast<const int32_t*>(row);
+        s = smem_lb(rid, (int)d, bj);
+        hit = s < d && rid[s] < bj1;
+      } else {
+        int64_t s64;
+        hit = send_msg(pool, p, d, bj, bj1, s64);
+        s = (int)s64;
+      }
+      if (hit) nch = pd - (s >> 2);
     }
-    while (todo) {
-      const int jj = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t c0 = __shfl_sync(0xffffffffu, s, jj) >> 2;  // first chunk of the message
-      const int64_t w0 = __shfl_sync(0xffffffffu, wi, jj) >> 2;
-      for (int64_t c = lane; c < pd - c0; c += 32) out4[w0 + c] = __ldg(&pool4[p0 + c0 + c]);
+    // slots of this step's messages: prefix over the row slots of each destination
+    int il = nch > 0, ic = nch;
+    for (int o = G; o < 32; o <<= 1) {
+      const int yl = __shfl_up_sync(FULL, il, o), yc = __shfl_up_sync(FULL, ic, o);
+      if (lane >= o) {
+        il += yl;
+        ic += yc;
+      }
+    }
+    if (nch > 0) out_len[run_l + (il - 1)] = (int32_t)(d - 4 * (s >> 2));
+    const long long dst0 = run_c + (ic - nch);
+    run_l += __shfl_sync(FULL, il, last);
+    run_c += __shfl_sync(FULL, ic, last);
+    const int c00 = s >> 2;  // first chunk of this lane's message inside its row
+    for (int jj = 0; jj < ndest; ++jj) {  // the group's lanes copy one message at a time
+      const int from = g * G + jj;
+      const int n = __shfl_sync(FULL, nch, from);
+      if (!__any_sync(FULL, n > 0)) continue;
+      const int c0 = __shfl_sync(FULL, c00, from);
+      const long long dc = __shfl_sync(FULL, dst0, from);
+      if (staged) {
+        for (int c = jl; c < n; c += G) out4[dc + c] = row[c0 + c];
+      } else {
+        const int4* src = pool4 + (p >> 2) + c0;
+        for (int c = jl; c < n; c += G) out4[dc + c] = __ldg(&src[c]);
+      }
     }
   }
 }
@@ -385,10 +488,12 @@ __global__ void k_sh_idx_count(const int64_t* __restrict__ pptr, const int32_t* 
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
     const int64_t p = pptr[r], d = len[r];
-    for (int64_t i = lane; i + 1 < d; i += 32) {
-      const int32_t u = pool[p + i];
+    for (int64_t b = 0; b + 1 < d; b += 32) {  // rows ascend: stop after the owned ids
+      const int64_t i = b + lane;
+      const int32_t u = (i + 1 < d) ? pool[p + i] : INT32_MAX;
       if (u >= lo && u < hi)
         atomicAdd(&acc[u - lo], (1ull << kCntShift) + (unsigned long long)(d - i - 1));
+      if (__all_sync(0xffffffffu, u >= hi)) break;
     }
   }
 }
@@ -418,8 +523,10 @@ __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* _
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
     const int64_t p = pptr[r], d = len[r];
-    for (int64_t i = lane; i + 1 < d; i += 32) {
-      const int32_t u = pool[p + i];
+    for (int64_t b = 0; b + 1 < d; b += 32) {
+      const int64_t i = b + lane;
+      const int32_t u = (i + 1 < d) ? pool[p + i] : INT32_MAX;
+      if (__all_sync(0xffffffffu, u >= hi)) break;
       if (u >= lo && u < hi) {
         const int64_t x = u - lo;
         const int64_t slot = rev_indptr[x] + atomicAdd(&cursor[x], 1);
@@ -720,18 +827,31 @@ int tc_shard_engine_cost_fin(const uint64_t* acc, const int32_t* effdeg, int64_t
   });
 }
 
+int tc_shard_send_plan_len(int64_t nrow, int32_t P, int64_t* len_host) {
+  return guarded([&] {
+    TC_REQUIRE(len_host != nullptr && P >= 1 && nrow >= 0, TC_EINVAL, "bad send plan query");
+    *len_host = 3 * (int64_t)P + 2 * (int64_t)P * send_blocks(nrow) * kSendWarps;
+  });
+}
+
 int tc_shard_send_sizes(const int64_t* indptr, const int32_t* indices, int64_t nrow, const int64_t* pool_indptr,
                         const int64_t* bounds, int32_t P, int32_t rank, int64_t* sizes_dev, int64_t* sizes_host,
                         tc_stream_t stream) {
   return guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
-    TC_REQUIRE(P >= 1 && P <= 32, TC_EINVAL, "the surrogate send supports P <= 32 ranks");
+    TC_REQUIRE(P >= 1 && P <= kEmitMaxP, TC_EINVAL, "the surrogate send supports P <= 32 ranks");
     TC_REQUIRE(rank >= 0 && rank < P, TC_EINVAL, "rank out of range");
-    TC_CUDA(cudaMemsetAsync(sizes_dev, 0, 3 * P * sizeof(int64_t), s));
-    if (nrow > 0) {
-      k_sh_send_count<<<grid_for(nrow * 32, kBlk, sm_count() * 8), kBlk, 0, s>>>(
-          indptr, indices, nrow, pool_indptr, bounds, P, rank, reinterpret_cast<long long*>(sizes_dev),
-          reinterpret_cast<long long*>(sizes_dev) + P, reinterpret_cast<long long*>(sizes_dev) + 2 * P);
+    const int nblk = send_blocks(nrow);
+    const int64_t nunit = (int64_t)nblk * kSendWarps;
+    TC_CUDA(cudaMemsetAsync(sizes_dev, 0, (3 * (size_t)P + 2 * (size_t)P * nunit) * sizeof(int64_t), s));
+    if (nrow > 0 && rank + 1 < P) {
+      long long* tot = reinterpret_cast<long long*>(sizes_dev);
+      long long* unit_l = tot + 3 * P;
+      long long* unit_w = unit_l + (int64_t)P * nunit;
+      k_sh_send_count<<<nblk, kBlk, 0, s>>>(indptr, indices, nrow, pool_indptr, bounds, P, rank,
+                                             send_group(P, rank), tot, unit_l, unit_w);
+      check_launch();
+      k_sh_send_prefix<<<1, 32 * P, 0, s>>>(tot, P, nunit, unit_l, unit_w);
       check_launch();
     }
     if (sizes_host) {
@@ -746,18 +866,16 @@ int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nr
                        int32_t* out_len, int32_t* out_ids, tc_stream_t stream) {
   return guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
-    TC_REQUIRE(P >= 1 && P <= 32, TC_EINVAL, "the surrogate send supports P <= 32 ranks");
+    TC_REQUIRE(P >= 1 && P <= kEmitMaxP, TC_EINVAL, "the surrogate send supports P <= 32 ranks");
     TC_REQUIRE(((uintptr_t)pool & 15) == 0 && ((uintptr_t)out_ids & 15) == 0, TC_EINVAL,
                "pool and out_ids must be 16-byte aligned");
-    if (nrow <= 0) return;
-    Scratch sc(s);
-    long long* off = sc.alloc<long long>(4 * P);
-    ex_sum(sc, reinterpret_cast<const long long*>(sizes_dev), off, P, s);
-    ex_sum(sc, reinterpret_cast<const long long*>(sizes_dev) + P, off + P, P, s);
-    TC_CUDA(cudaMemsetAsync(off + 2 * P, 0, 2 * P * sizeof(long long), s));
-    k_sh_send_emit<<<grid_for(nrow * 32, kBlk, sm_count() * 8), kBlk, 0, s>>>(
-        indptr, indices, nrow, pool_indptr, reinterpret_cast<const int4*>(pool), bounds, P, rank, off, off + P,
-        reinterpret_cast<unsigned long long*>(off + 2 * P), out_len, reinterpret_cast<int4*>(out_ids));
+    if (nrow <= 0 || rank + 1 >= P) return;
+    const int nblk = send_blocks(nrow);
+    const long long* base_l = reinterpret_cast<const long long*>(sizes_dev) + 3 * P;
+    const long long* base_w = base_l + (int64_t)P * nblk * kSendWarps;
+    k_sh_send_emit<<<nblk, kBlk, 0, s>>>(indptr, indices, nrow, pool_indptr, reinterpret_cast<const int4*>(pool),
+                                          bounds, P, rank, send_group(P, rank), base_l, base_w, out_len,
+                                          reinterpret_cast<int4*>(out_ids));
     check_launch();
   });
 }

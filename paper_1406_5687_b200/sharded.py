@@ -22,9 +22,10 @@ pairs, and
           7. exchange    per destination j > r (LastProc, _kernels.py:94-126)
                          the suffix of N^_v at or above b_j (from its 16-byte
                          chunk of the padded pool), padded, in
-                         bounded rounds (peers r+1.. r+t); each round's lists
-                         are indexed and counted on the device while the next
-                         round is in flight
+                         bounded rounds (a round = a group of consecutive
+                         sender ranks); each round's lists are indexed and
+                         counted on the device while the next round is in
+                         flight
           8. reduce      all_reduce(SUM) of the uint64 partials
                          (reduce_sum, runtime.py:255-259)
 
@@ -220,7 +221,9 @@ class ShardOps:
         hit = sh.cache.get(("send_sizes", P, rank))
         if hit is not None:
             return hit
-        sizes = torch.empty(3 * P, dtype=torch.int64, device=self.dev)
+        plen = ctypes.c_int64()
+        self.L.call("tc_shard_send_plan_len", sh.hi - sh.lo, int(P), ctypes.byref(plen))
+        sizes = torch.empty(plen.value, dtype=torch.int64, device=self.dev)  # sizes + the pack's block plan
         host = np.zeros(3 * P, np.int64)
         b = sh.cache.get("bounds_dev")
         if b is None:
@@ -250,7 +253,9 @@ class ShardOps:
             # planning (index + tier lists; it synchronises its own stream) and
             # engine runs go to side streams, so neither holds back the
             # collectives issued on the current stream
-            st = self._st = (torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev))
+            st = self._st = (torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev),
+                             torch.cuda.Stream(device=self.dev))
+            self._turn = 0
         return st
 
     def _plan(self, sh, row_len, pool):
@@ -273,8 +278,13 @@ class ShardOps:
         return _PlanHandle(h, (pip, rip, rseg, rcost, pool, row_len))
 
     def _launch(self, plan):
-        """One engine run of a plan on the run stream; returns its output."""
-        _, run_s = self._streams()
+        """One engine run of a plan on a run stream; returns its output.
+        Consecutive runs alternate between two streams, so a run's tail (the
+        last chunks of its hubs) overlaps the start of the next one."""
+        st = self._streams()
+        self._turn ^= 1
+        run_s = st[1 + self._turn]
+        run_s.wait_stream(st[0])  # the plan was built on the plan stream
         with torch.cuda.stream(run_s):
             o = torch.empty(1, dtype=torch.int64, device=self.dev)
             self.L.call("tc_plan_run", plan.handle, self.L.ptr(o), self.L.stream())
@@ -284,7 +294,7 @@ class ShardOps:
         """Engine run over the shard's own lists (plan cached on the shard)."""
         plan = sh.cache.get("local_plan")
         if plan is None:
-            plan_s, _ = self._streams()
+            plan_s = self._streams()[0]
             plan_s.wait_stream(torch.cuda.current_stream(self.dev))
             with torch.cuda.stream(plan_s):
                 row_len = (sh.indptr[1:] - sh.indptr[:-1]).to(torch.int32).contiguous()
@@ -295,7 +305,7 @@ class ShardOps:
         """Index + plan the received padded lists on the plan stream (after
         the current stream, which their transfer completed on), run them on
         the run stream.  Returns (out, plan): keep the plan until finish."""
-        plan_s, _ = self._streams()
+        plan_s = self._streams()[0]
         plan_s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(plan_s):
             plan = self._plan(sh, row_len, pool)
@@ -303,8 +313,8 @@ class ShardOps:
 
     def finish(self, outs):
         """Sum of the run outputs, read after the run stream's work."""
-        _, run_s = self._streams()
-        torch.cuda.current_stream(self.dev).wait_stream(run_s)
+        for st in self._streams()[1:]:
+            torch.cuda.current_stream(self.dev).wait_stream(st)
         return int(sum(int(o.item()) for o in outs))
 
 # ------------------------------------------------------------------ collectives
@@ -561,7 +571,7 @@ def build_gen(pairs, pos_base, P, rank, cost="predsum", ops=None, keep_maps=Fals
     c = ops.predsum(lohi, effdeg, n)
     c = yield ("allreduce", c, "sum")
     bounds = ops.balanced(c, n, P)
-    del c
+    weights = c
     # 5. the shard: pairs to the owner of lo
     routed, counts = ops.route(lohi, bounds, P)
     del lohi
@@ -579,7 +589,7 @@ def build_gen(pairs, pos_base, P, rank, cost="predsum", ops=None, keep_maps=Fals
         ec = ops.engine_cost(acc, effdeg, n, TAB_WEIGHT, SEND_WEIGHT)
         del acc
         nb = ops.balanced(ec, n, P)
-        del ec
+        weights = ec
         indptr, indices = yield from _repartition(indptr, indices, lo, hi, nb, P, dev)
         bounds = nb
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
@@ -588,6 +598,9 @@ def build_gen(pairs, pos_base, P, rank, cost="predsum", ops=None, keep_maps=Fals
     del effdeg
     pip, pool = ops.pool(indptr, indices)
     sh = ShardGraph(lo, hi, n, m, np.asarray(bounds, np.int64), indptr, indices, pip, pool)
+    # the per-node weights the partition was cut by (replicated, O(n)): the
+    # measured refinement (rebalance_gen) rescales them
+    sh.cache["weights"] = weights
     if keep_maps:
         sh.relabel, sh.orig_ids = relabel, orig_ids
     return sh
@@ -610,6 +623,43 @@ def _repartition(indptr, indices, lo, hi, nb, P, dev):
     if rl.numel():
         nip[1:] = torch.cumsum(rl.to(torch.int64), 0)
     return nip, ri
+
+
+def rebalance_gen(sh: ShardGraph, P, rank, busy_ms, ops=None):
+    """Measured refinement of the partition (the cost-function partition of
+    partitioning.py:79-141 with the cost taken from a run instead of a
+    model): every rank reports the device time of its last count, the node
+    weights of rank r's range are scaled by time_r / weight_r (so the weight
+    of a range is the time it took), the bounds are re-balanced on the scaled
+    weights and the rows whose owner changed move (one all_to_all of row
+    lengths and one of ids).  Returns the new ShardGraph; the old one is
+    consumed."""
+    ops = ops or ShardOps()
+    dev = sh.indptr.device
+    w = sh.cache.get("weights")
+    if w is None:
+        raise ValueError("the shard carries no partition weights")
+    t = torch.zeros(P, dtype=torch.int64, device=dev)
+    t[rank] = max(1, int(round(1e3 * float(busy_ms))))  # microseconds
+    t = yield ("allreduce", t, "sum")
+    b = torch.as_tensor(np.asarray(sh.bounds, np.int64)).to(dev)
+    wf = w.to(torch.float64)
+    pre = torch.cat([torch.zeros(1, dtype=torch.float64, device=dev), torch.cumsum(wf, 0)])
+    tot = pre[b[1:]] - pre[b[:-1]]
+    scale = t.to(torch.float64) / torch.clamp(tot, min=1.0)
+    owner = torch.bucketize(torch.arange(sh.n, device=dev), b[1:-1].contiguous(), right=True)
+    wf = wf * scale[owner]
+    # integer weights again (tc_balanced_bounds), ~2^44 in total
+    wn = torch.clamp((wf * (float(1 << 44) / max(float(wf.sum()), 1.0))).round(), min=0).to(torch.int64)
+    del wf, pre, owner
+    nb = ops.balanced(wn, sh.n, P)
+    indptr, indices = yield from _repartition(sh.indptr, sh.indices, sh.lo, sh.hi, nb, P, dev)
+    lo, hi = int(nb[rank]), int(nb[rank + 1])
+    pip, pool = ops.pool(indptr, indices)
+    out = ShardGraph(lo, hi, sh.n, sh.m, np.asarray(nb, np.int64), indptr, indices, pip, pool, sh.relabel, sh.orig_ids)
+    out.cache["weights"] = wn
+    sh.cache.clear()
+    return out
 
 
 def _phase(prof, name, t0):
@@ -654,22 +704,23 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
         rsz, _ = yield ("a2a", st, np.ones(P, np.int64))
         rsz = rsz.cpu().numpy() if isinstance(rsz, torch.Tensor) else np.asarray(rsz)
         rlists, rwords = rsz[:, 0], rsz[:, 1]
-        # rounds over peer distance t: sends to rank + t, receives from
-        # rank - t; a round closes once the largest receive volume (over
-        # ranks) would pass round_words -- the same grouping on every rank
-        vol = torch.zeros(P, dtype=torch.int64, device=dev)
-        for t in range(1, P):
-            if rank - t >= 0:
-                vol[t] = int(rwords[rank - t])
+        # rounds over sender ranks: in a round the ranks of a consecutive
+        # group send all their messages and every rank above them receives;
+        # a group closes once the largest receive volume it could cause (the
+        # sum over its senders of their largest message set) would pass
+        # round_words -- the same grouping on every rank
+        hv = np.zeros(P, np.int64)
+        hv[:rank] = np.asarray(rwords, np.int64)[:rank]
+        vol = torch.as_tensor(hv).to(dev)
         vol = yield ("allreduce", vol, "max")
         vol = vol.cpu().numpy()
         rounds, cur, acc = [], [], 0
-        for t in range(1, P):
-            w = int(vol[t])
+        for s_ in range(P - 1):
+            w = int(vol[s_])
             if cur and acc + w > round_words:
                 rounds.append(cur)
                 cur, acc = [], 0
-            cur.append(t)
+            cur.append(s_)
             acc += w
         if cur:
             rounds.append(cur)
@@ -679,21 +730,19 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
     rlists, rwords, rounds = xplan
     lens, ids = ops.send_pack(sh, P, rank, sizes_dev, int(lists.sum()), int(words.sum()))
     tp = _phase(prof, "pack", tp)
-    loff = np.concatenate([[0], np.cumsum(lists)])
-    woff = np.concatenate([[0], np.cumsum(words)])
     met.wire_bytes = int(4 * (lists.sum() + words.sum()) + 16 * P)
     pending = None
     for rd in rounds:
         sl, sw = np.zeros(P, np.int64), np.zeros(P, np.int64)
         rl, rw = np.zeros(P, np.int64), np.zeros(P, np.int64)
-        for t in rd:
-            if rank + t < P:
-                sl[rank + t], sw[rank + t] = lists[rank + t], words[rank + t]
-            if rank - t >= 0:
-                rl[rank - t], rw[rank - t] = rlists[rank - t], rwords[rank - t]
-        sel = [j for j in range(P) if sl[j]]
-        send_l = torch.cat([lens[int(loff[j]): int(loff[j + 1])] for j in sel]) if sel else lens[:0]
-        send_w = torch.cat([ids[int(woff[j]): int(woff[j + 1])] for j in sel]) if sel else ids[:0]
+        if rank in rd:  # this rank's turn: all its messages, grouped by destination
+            sl[rank + 1:], sw[rank + 1:] = lists[rank + 1:], words[rank + 1:]
+            send_l, send_w = lens, ids
+        else:
+            send_l, send_w = lens[:0], ids[:0]
+        for s_ in rd:
+            if s_ < rank:
+                rl[s_], rw[s_] = rlists[s_], rwords[s_]
         buf, rpool = ops.recv_pool(int(rw.sum()))
         h_l = yield ("a2a_start", send_l, sl, rl, None)
         h_w = yield ("a2a_start", send_w, sw, rw, rpool)
@@ -745,6 +794,21 @@ def count_sharded(sh: ShardGraph, group=None, ops=None, round_words=1 << 27):
 
     P, rank = dist.get_world_size(group), dist.get_rank(group)
     return run_dist(count_gen(sh, P, rank, ops, round_words), group)
+
+
+def rebalance_sharded(sh: ShardGraph, busy_ms, group=None, ops=None):
+    """Measured refinement of the partition on this rank (see rebalance_gen)."""
+    import torch.distributed as dist
+
+    P, rank = dist.get_world_size(group), dist.get_rank(group)
+    return run_dist(rebalance_gen(sh, P, rank, busy_ms, ops), group)
+
+
+def emulate_rebalance(shards, busy_ms, ops=None):
+    """All P ranks of the measured refinement in this process."""
+    P = len(shards)
+    res, _ = emulate([rebalance_gen(sh, P, r, busy_ms[r], ops) for r, sh in enumerate(shards)])
+    return res
 
 
 def emulate_build(raw, P, cost="predsum", ops=None, keep_maps=False, timed=False):

@@ -63,6 +63,39 @@ def test_sharded_protocol_emulated_numpy(name):
         assert S.emulate_count(eshards, ops=ops)[0] == int(case["T"][0])
 
 
+def _check_rebalanced(case, shards, P):
+    """Ranges tile [0, n), every rank holds exactly the reference rows of its
+    range, partials sum to T."""
+    ip, ix = case["eff_indptr"], case["eff_indices"]
+    b = shards[0].bounds.tolist()
+    assert b[0] == 0 and b[-1] == len(case["relabel"]) and all(x <= y for x, y in zip(b, b[1:]))
+    for r, sh in enumerate(shards):
+        assert sh.bounds.tolist() == b and (sh.lo, sh.hi) == (b[r], b[r + 1])
+        assert np.array_equal(sh.indptr.cpu().numpy(), ip[sh.lo: sh.hi + 1] - ip[sh.lo])
+        assert np.array_equal(sh.indices.cpu().numpy(), ix[ip[sh.lo]: ip[sh.hi]])
+
+
+@pytest.mark.parametrize("name", ["pa_500_8_11", "gnm_2000_16000"])
+def test_sharded_rebalance_emulated_numpy(name):
+    """The measured refinement: skewed rank times move the bounds towards
+    the slow rank's side, the shards stay the reference's rows and the count
+    stays T."""
+    case = SMALL[name]
+    raw = torch.as_tensor(case["raw"].astype(np.int32))
+    ops = NumpyShardOps()
+    for P in (2, 3):
+        shards, _ = S.emulate_build(raw, P, cost="engine", ops=ops)
+        b0 = shards[0].bounds.tolist()
+        shards = S.emulate_rebalance(shards, [10.0] + [1.0] * (P - 1), ops=ops)  # rank 0 was slow
+        _check_rebalanced(case, shards, P)
+        assert shards[0].bounds[1] < b0[1]
+        tot, mets, _ = S.emulate_count(shards, ops=ops, round_words=64)
+        assert tot == int(case["T"][0]) and sum(m.triangles for m in mets) == tot
+        shards = S.emulate_rebalance(shards, [1.0] * P, ops=ops)  # equal times: weights already balanced
+        _check_rebalanced(case, shards, P)
+        assert S.emulate_count(shards, ops=ops)[0] == int(case["T"][0])
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -139,6 +172,9 @@ def test_sharded_device_emulated(name):
             _check_count(case, tot, mets, P)
         eshards, _ = S.emulate_build(raw, P, cost="engine")
         assert S.emulate_count(eshards)[0] == int(case["T"][0])
+        eshards = S.emulate_rebalance(eshards, [float(1 + (r % 3)) for r in range(P)])
+        _check_rebalanced(case, eshards, P)
+        assert S.emulate_count(eshards, round_words=64)[0] == int(case["T"][0])
 
 
 @pytest.mark.gpu

@@ -22,6 +22,8 @@ ap.add_argument("--ranks", default="2,4,8")
 ap.add_argument("--costs", default="predsum,engine")
 ap.add_argument("--round-words", type=int, default=1 << 27)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--rebalance", type=int, default=2, help="measured refinements of the partition after the first count")
+ap.add_argument("--no-prof", action="store_true")
 a = ap.parse_args()
 raw = bench.host_raw_edges(a.config, pin=True)
 g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw)))
@@ -41,18 +43,23 @@ for cost in a.costs.split(","):
         t0 = time.perf_counter()
         shards, bms = S.emulate_build(dev_raw, P, cost=cost, timed=True)
         tb = time.perf_counter() - t0
-        best = None
-        for _ in range(a.reps):
-            tot, mets, ms = S.emulate_count(shards, round_words=a.round_words, timed=True)
-            assert tot == T, (tot, T)
-            best = ms if best is None else [min(x, y) for x, y in zip(best, ms)]  # per-rank minimum
-        res = [sh.resident_bytes() / 2**20 for sh in shards]
-        print(f"{a.config} P={P} cost={cost}: count ranks ms {' '.join(f'{x:.2f}' for x in best)} max {max(best):.2f} "
-              f"(sum {sum(best):.1f}) -> eff {t1 / (P * max(best)):.2f}; build ranks ms max {max(bms):.1f} (wall {tb:.1f}s); "
-              f"resident MiB max {max(res):.0f}; partials {[m.triangles for m in mets]}", flush=True)
-        profs = [dict() for _ in range(P)]
-        S.emulate_count(shards, round_words=a.round_words, profs=profs)
-        for r, pr in enumerate(profs):
-            print(f"   rank {r}: " + " ".join(f"{k} {v:.2f}" for k, v in pr.items() if k != "start"), flush=True)
+        for it in range(a.rebalance + 1):
+            best = None
+            for _ in range(a.reps):
+                tot, mets, ms = S.emulate_count(shards, round_words=a.round_words, timed=True)
+                assert tot == T, (tot, T)
+                best = ms if best is None else [min(x, y) for x, y in zip(best, ms)]  # per-rank minimum
+            res = [sh.resident_bytes() / 2**20 for sh in shards]
+            tag = f"cost={cost}" + (f" +{it} measured refinement(s)" if it else "")
+            print(f"{a.config} P={P} {tag}: count ranks ms {' '.join(f'{x:.2f}' for x in best)} max {max(best):.2f} "
+                  f"(sum {sum(best):.1f}) -> eff {t1 / (P * max(best)):.2f}; build ranks ms max {max(bms):.1f} (wall {tb:.1f}s); "
+                  f"resident MiB max {max(res):.0f}; bounds {shards[0].bounds.tolist()}", flush=True)
+            if it < a.rebalance:
+                shards = S.emulate_rebalance(shards, best)
+        if not a.no_prof:
+            profs = [dict() for _ in range(P)]
+            S.emulate_count(shards, round_words=a.round_words, profs=profs)
+            for r, pr in enumerate(profs):
+                print(f"   rank {r}: " + " ".join(f"{k} {v:.2f}" for k, v in pr.items() if k != "start"), flush=True)
         del shards
         torch.cuda.empty_cache()
