@@ -459,11 +459,13 @@ def device_raw_edges(cfg):
     return rmat_edges(c["scale"], c["ef"], c["seed"])
 
 
-def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_words=1 << 27):
+def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_words=1 << 28, refinements=2):
     """The paper's space-efficient scheme end to end on N GPUs (sharded.py):
     each rank keeps only its slice of the raw pairs, builds only its node
     range (distributed normalize + build_graph), and the count exchanges
-    suffix lists in bounded rounds; device time, max over ranks."""
+    suffix lists in bounded rounds; device time, max over ranks.  The
+    partition is cut by the cost model (`cost`), then refined `refinements`
+    times from the ranks' measured device time (sharded.rebalance_gen)."""
     import torch
     import torch.distributed as dist
 
@@ -479,6 +481,7 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
     builds = []
     sh = None
     for i in range(2):
+        sh = None
         barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -488,25 +491,50 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
         builds.append(s.elapsed_time(e))
     del sl
     torch.cuda.empty_cache()
-    for _ in range(warmup):
-        T, met = S.count_sharded(sh, round_words=round_words)
-    times = []
-    for _ in range(steps):
-        barrier()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        T, met = S.count_sharded(sh, round_words=round_words)
-        e.record()
-        torch.cuda.synchronize()
-        times.append(s.elapsed_time(e))
-    ms = max_over_ranks(statistics.median(times))
+    ops = S.ShardOps()
+
+    def timed_counts(k):
+        ts = []
+        for _ in range(k):
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            T, met = S.count_sharded(sh, ops=ops, round_words=round_words)
+            e.record()
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        return ts, T, met
+
+    cold, T, met = timed_counts(1)  # builds the send plan, the exchange plan and the engine plans
+    trail = []
+    rebal_ms = []
+    for it in range(refinements + 1):
+        timed_counts(warmup)
+        ops.timing = True
+        ops.busy_ms()
+        ts, T, met = timed_counts(steps)
+        busy = ops.busy_ms() / steps
+        ops.timing = False
+        trail.append({"count_ms": max_over_ranks(statistics.median(ts)), "rank_busy_ms_max": max_over_ranks(busy),
+                      "bounds": [int(x) for x in sh.bounds]})
+        if it < refinements:
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            sh = S.rebalance_sharded(sh, busy, ops=ops)
+            e.record()
+            torch.cuda.synchronize()
+            rebal_ms.append(max_over_ranks(s.elapsed_time(e)))
+            timed_counts(1)
+    ms = trail[-1]["count_ms"]
     bms = max_over_ranks(min(builds))
     res = max_over_ranks(float(sh.resident_bytes()))
     want, src = golden_T(cfg)
     out = {"workload": CONFIGS[cfg]["desc"], "n": sh.n, "m": sh.m, "m_raw": m_raw, "n_gpus": world,
-           "mode": f"sharded surrogate ({cost} partition)", "triangles": T, "triangles_golden": want,
-           "triangles_ok": (want == T) if want is not None else None, "count_ms": ms,
-           "edges_per_s": sh.m / (ms / 1e3), "build_ms": bms, "max_rank_resident_bytes": res,
+           "mode": f"sharded surrogate ({cost} partition + {len(trail) - 1} measured refinement(s))", "triangles": T,
+           "triangles_golden": want, "triangles_ok": (want == T) if want is not None else None, "count_ms": ms,
+           "edges_per_s": sh.m / (ms / 1e3), "count_cold_ms": max_over_ranks(cold[0]), "refinement_trail": trail,
+           "rebalance_ms": rebal_ms, "build_ms": bms, "max_rank_resident_bytes": res,
            "rank_partial": met.triangles, "round_words": round_words}
     del sh
     torch.cuda.empty_cache()

@@ -167,6 +167,12 @@ int tc_plan_middle(const int64_t* tab_indptr, const int32_t* tab_indices, const 
                    int64_t n, int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                    tc_plan_t* plan, tc_stream_t stream);
 int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream);
+/* Points the plan at another copy of the segment array and the pool with the
+ * same structure (same owners, same segments per owner, same segment
+ * lengths per owner up to their order): the sharded count's received lists
+ * arrive in fresh buffers at every count (tc_shard_index_emit).  Host-side
+ * only; runs issued afterwards use the new arrays. */
+int tc_plan_rebind(tc_plan_t plan, const int32_t* rev_seg, const int32_t* pool);
 int tc_plan_free(tc_plan_t plan);
 
 /* Interleaved split of one plan across `nparts` devices that each hold the
@@ -456,6 +462,13 @@ int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nr
 int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
                    const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr, int32_t* rev_seg,
                    int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream);
+
+/* The scatter pass of tc_shard_index for rows whose per-owner offsets
+ * rev_indptr are kept from an earlier call on lists of the same structure
+ * (the same exchange round of the same partitioned graph): fills
+ * pool_indptr and rev_seg only. */
+int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
+                        const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg, tc_stream_t stream);
 
 /* ------------------------------------------------------------ NCCL layer */
 

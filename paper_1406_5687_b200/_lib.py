@@ -35,6 +35,7 @@ _SIGS = {
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_plan_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_vp), _vp],
     "tc_plan_run": [_vp, _vp, _vp],
+    "tc_plan_rebind": [_vp, _vp, _vp],
     "tc_plan_middle_parts": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, _i32,
                              ctypes.POINTER(_vp), _vp],
     "tc_plan_run_part": [_vp, _i32, _vp, _vp],
@@ -75,6 +76,7 @@ _SIGS = {
     "tc_shard_send_sizes": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
     "tc_shard_send_pack": [_vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
     "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
+    "tc_shard_index_emit": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp],
     "tc_nccl_unique_id": [_vp],
     "tc_nccl_init_rank": [_vp, _i32, _i32, ctypes.POINTER(_vp)],
     "tc_nccl_init_all": [_i32, _vp, _vp],

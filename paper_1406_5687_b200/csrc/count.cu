@@ -2076,6 +2076,17 @@ int tc_plan_run(tc_plan_t plan, unsigned long long* out, tc_stream_t stream) {
   return tc_plan_run_part(plan, -1, out, stream);
 }
 
+int tc_plan_rebind(tc_plan_t plan, const int32_t* rev_seg, const int32_t* pool) {
+  return tcb::guarded([&] {
+    TC_REQUIRE(plan != nullptr && rev_seg != nullptr && pool != nullptr, TC_EINVAL, "NULL plan or array");
+    TC_REQUIRE(((uintptr_t)pool & 15) == 0, TC_EINVAL, "pool must be 16-byte aligned");
+    auto* P = reinterpret_cast<tcb::MiddlePlan*>(plan);
+    P->rev_seg = rev_seg;
+    P->pool = pool;
+    for (int k = 0; k < 3; ++k) P->L.args[k].pool = pool;  // launch arguments are copied at each run
+  });
+}
+
 int tc_plan_free(tc_plan_t plan) {
   return tcb::guarded([&] { delete reinterpret_cast<tcb::MiddlePlan*>(plan); });
 }

@@ -516,6 +516,12 @@ __global__ void k_sh_idx_rows(const unsigned long long* __restrict__ acc, const 
   }
 }
 
+// cursor[x] = rev_indptr[x]: the emit pass then takes a segment's slot with
+// one atomic (segments < 2^31: they index an int32 pool)
+__global__ void k_sh_idx_cursor(const int64_t* __restrict__ rev_indptr, int64_t nx, int32_t* cursor) {
+  GRID_STRIDE(x, nx) cursor[x] = (int32_t)rev_indptr[x];
+}
+
 __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* __restrict__ len, int64_t nrow,
                               const int32_t* __restrict__ pool, int64_t lo, int64_t hi,
                               const int64_t* __restrict__ rev_indptr, int32_t* cursor, int2* rev_seg) {
@@ -529,9 +535,9 @@ __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* _
       if (__all_sync(0xffffffffu, u >= hi)) break;
       if (u >= lo && u < hi) {
         const int64_t x = u - lo;
-        const int64_t slot = rev_indptr[x] + atomicAdd(&cursor[x], 1);
+        const int64_t slot = atomicAdd(&cursor[x], 1);
 #if TCB_DEBUG
-        assert(slot < rev_indptr[x + 1]);
+        assert(slot >= rev_indptr[x] && slot < rev_indptr[x + 1]);
 #endif
         rev_seg[slot] = make_int2((int)(p + i + 1), (int)(p + d));
       }
@@ -907,13 +913,42 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
     ex_sum(sc, cnt, rev_indptr, nx + 1, s);
     ex_sum(sc, cost, rev_cost, nx + 1, s);
     int32_t* cur = sc.alloc<int32_t>(nx + 1);
-    TC_CUDA(cudaMemsetAsync(cur, 0, (nx + 1) * sizeof(int32_t), s));
+    k_sh_idx_cursor<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(rev_indptr, nx, cur);
+    check_launch();
     if (nrow > 0) {
       k_sh_idx_emit<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
                                           reinterpret_cast<int2*>(rev_seg));
       check_launch();
     }
     if (nseg_host) *nseg_host = scalar_of(rev_indptr + nx, s);
+  });
+}
+
+// The scatter pass of tc_shard_index alone, for rows whose owner offsets
+// (rev_indptr) are already known: a round of the exchange delivers the same
+// lists at every count of a partitioned graph, so the per-owner counts, the
+// cost prefix and the engine plan built from them are kept and only the
+// segments are scattered again.
+int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
+                        const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg, tc_stream_t stream) {
+  return guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    TC_REQUIRE(lo >= 0 && lo <= hi, TC_EINVAL, "bad owner range");
+    const int64_t nx = hi - lo;
+    Scratch sc(s);
+    int64_t* sz = sc.alloc<int64_t>(nrow + 1);
+    k_sh_len_sizes<<<grid_for(nrow + 1, kBlk), kBlk, 0, s>>>(row_len, nrow, sz);
+    check_launch();
+    ex_sum(sc, sz, pool_indptr, nrow + 1, s);
+    int32_t* cur = sc.alloc<int32_t>(nx + 1);
+    k_sh_idx_cursor<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(rev_indptr, nx, cur);
+    check_launch();
+    if (nrow > 0) {
+      const int grid = grid_for(nrow * 32, kBlk, sm_count() * 16);
+      k_sh_idx_emit<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
+                                          reinterpret_cast<int2*>(rev_seg));
+      check_launch();
+    }
   });
 }
 

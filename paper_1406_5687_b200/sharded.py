@@ -108,6 +108,32 @@ class ShardOps:
 
         self.L = _lib
         self.dev = device or _lib.device()
+        # timing = True brackets the rank's own device work (pack, receive
+        # index, engine runs) with CUDA events on the streams it runs on;
+        # busy_ms() is their sum -- the rank's cost for rebalance_gen, free of
+        # the time spent waiting for peers
+        self.timing = False
+        self._busy = []
+
+    def _tic(self, stream=None):
+        if not self.timing:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream or torch.cuda.current_stream(self.dev))
+        return e
+
+    def _toc(self, e0, stream=None):
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream or torch.cuda.current_stream(self.dev))
+            self._busy.append((e0, e1))
+
+    def busy_ms(self):
+        """Device time of the bracketed work since the last call."""
+        torch.cuda.synchronize(self.dev)
+        t = sum(a.elapsed_time(b) for a, b in self._busy)
+        self._busy = []
+        return t
 
     # -- build --
     def minmax(self, pairs):
@@ -237,9 +263,11 @@ class ShardOps:
     def send_pack(self, sh, P, rank, sizes_dev, nl, nw):
         lens = torch.empty(max(nl, 1), dtype=torch.int32, device=self.dev)
         ids = torch.empty(max(nw, 4), dtype=torch.int32, device=self.dev)
+        t0 = self._tic()
         self.L.call("tc_shard_send_pack", self.L.ptr(sh.indptr), self.L.ptr(sh.indices), sh.hi - sh.lo,
                     self.L.ptr(sh.pool_indptr), self.L.ptr(sh.pool), self.L.ptr(sh.cache["bounds_dev"]), int(P),
                     int(rank), self.L.ptr(sizes_dev), self.L.ptr(lens), self.L.ptr(ids), self.L.stream())
+        self._toc(t0)
         return lens[:nl], ids[:nw]
 
     def recv_pool(self, nw):
@@ -287,7 +315,9 @@ class ShardOps:
         run_s.wait_stream(st[0])  # the plan was built on the plan stream
         with torch.cuda.stream(run_s):
             o = torch.empty(1, dtype=torch.int64, device=self.dev)
+            t0 = self._tic(run_s)
             self.L.call("tc_plan_run", plan.handle, self.L.ptr(o), self.L.stream())
+            self._toc(t0, run_s)
         return o
 
     def start_local(self, sh):
@@ -301,15 +331,47 @@ class ShardOps:
                 plan = sh.cache["local_plan"] = self._plan(sh, row_len, sh.pool)
         return self._launch(plan), plan
 
-    def count_received(self, sh, row_len, pool):
+    def count_received(self, sh, row_len, pool, key=None):
         """Index + plan the received padded lists on the plan stream (after
         the current stream, which their transfer completed on), run them on
-        the run stream.  Returns (out, plan): keep the plan until finish."""
+        a run stream.  Returns (out, plan): keep the plan until finish.
+
+        key names the exchange round: a round delivers lists of the same
+        structure at every count of a partitioned graph (the pack is
+        deterministic), so the per-owner offsets, the cost prefix and the
+        engine plan (all O(owned nodes)) are kept on the shard after the
+        first count; later counts only scatter the segments of the fresh
+        lists (tc_shard_index_emit) and point the plan at them."""
+        L = self.L
         plan_s = self._streams()[0]
         plan_s.wait_stream(torch.cuda.current_stream(self.dev))
+        hit = sh.cache.get(("recv_plan", key)) if key is not None else None
         with torch.cuda.stream(plan_s):
-            plan = self._plan(sh, row_len, pool)
+            t0 = self._tic(plan_s)
+            if hit is None or hit[1] != (int(row_len.numel()), int(pool.numel())):
+                plan = self._plan(sh, row_len, pool)
+                if key is not None:
+                    sh.cache[("recv_plan", key)] = (plan, (int(row_len.numel()), int(pool.numel())))
+            else:
+                plan = hit[0]
+                nrow = int(row_len.numel())
+                pip = torch.empty(nrow + 1, dtype=torch.int64, device=self.dev)
+                rseg = torch.empty(2 * max(int(pool.numel()), 1), dtype=torch.int32, device=self.dev)
+                rip = plan.keep[1]
+                L.call("tc_shard_index_emit", L.ptr(row_len), nrow, L.ptr(pool), sh.lo, sh.hi, L.ptr(rip), L.ptr(pip),
+                       L.ptr(rseg), L.stream())
+                L.call("tc_plan_rebind", plan.handle, L.ptr(rseg), L.ptr(pool))
+                # the plan's handle keeps the offsets and costs; this count's arrays live until finish
+                plan.keep = (pip, rip, rseg, plan.keep[3], pool, row_len)
+            self._toc(t0, plan_s)
         return self._launch(plan), plan
+
+    def release_received(self, plan):
+        """Drops a received round's arrays from its (kept) plan once the
+        count has finished: between counts a rank holds only its shard and
+        the O(owned nodes) offsets, costs and plan of each round."""
+        k = plan.keep
+        plan.keep = (None, k[1], None, k[3], None, None)
 
     def finish(self, outs):
         """Sum of the run outputs, read after the run stream's work."""
@@ -451,11 +513,15 @@ def run_capi(gen, comm: CComm):
             raise ValueError(f"unknown collective {kind}")
 
 
-def emulate(gens, timed=False):
+def emulate(gens, timed=False, busy=None):
     """Runs P rank generators in lockstep in this process (one device): every
     collective is performed once all ranks have reached it.  With timed=True
-    each rank's device work between collectives is bracketed by CUDA events;
-    returns (results, per-rank device ms)."""
+    each rank's device work between collectives is bracketed by CUDA events
+    (host gaps between its kernels included); returns (results, per-rank
+    device ms).  busy (a list of P zeros) collects, per rank, the event
+    brackets of its own kernels (ShardOps.busy_ms: pack, receive index,
+    engine runs) -- the measure bench.py's N-GPU run feeds to the
+    refinement."""
     P = len(gens)
     res = [None] * P
     done = [False] * P
@@ -472,11 +538,14 @@ def emulate(gens, timed=False):
                 torch.cuda.synchronize()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
+            o = ops_of(gens[r]) if busy is not None else None
             try:
                 reqs[r] = gens[r].send(res[r])
             except StopIteration as stop:
                 done[r] = True
                 out[r] = stop.value
+            if o is not None and getattr(o, "timing", False):
+                busy[r] += o.busy_ms()
             if timed:
                 # the segment's side-stream work (engine runs, planning) is
                 # counted with it: per-rank time is serialised (no overlap
@@ -672,7 +741,7 @@ def _phase(prof, name, t0):
     return t
 
 
-def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, prof=None):
+def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 28, met=None, prof=None):
     """One rank of the count (steps 6-8); returns (total, RankMetrics).
     round_words bounds the padded ids a rank receives per exchange round.
     prof (a dict, profiling only) collects synchronised per-phase times."""
@@ -706,22 +775,21 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
         rlists, rwords = rsz[:, 0], rsz[:, 1]
         # rounds over sender ranks: in a round the ranks of a consecutive
         # group send all their messages and every rank above them receives;
-        # a group closes once the largest receive volume it could cause (the
-        # sum over its senders of their largest message set) would pass
-        # round_words -- the same grouping on every rank
-        hv = np.zeros(P, np.int64)
-        hv[:rank] = np.asarray(rwords, np.int64)[:rank]
-        vol = torch.as_tensor(hv).to(dev)
-        vol = yield ("allreduce", vol, "max")
-        vol = vol.cpu().numpy()
-        rounds, cur, acc = [], [], 0
+        # a group closes once the largest volume a rank would receive in it
+        # would pass round_words -- the same grouping on every rank (from the
+        # replicated P x P volume matrix)
+        hv = np.zeros((P, P), np.int64)
+        hv[rank, :rank] = np.asarray(rwords, np.int64)[:rank]
+        vol = torch.as_tensor(hv.reshape(-1)).to(dev)
+        vol = yield ("allreduce", vol, "sum")
+        vol = (vol.cpu().numpy() if isinstance(vol, torch.Tensor) else np.asarray(vol)).reshape(P, P)
+        rounds, cur, acc = [], [], np.zeros(P, np.int64)
         for s_ in range(P - 1):
-            w = int(vol[s_])
-            if cur and acc + w > round_words:
+            if cur and int((acc + vol[:, s_]).max()) > round_words:
                 rounds.append(cur)
-                cur, acc = [], 0
+                cur, acc = [], np.zeros(P, np.int64)
             cur.append(s_)
-            acc += w
+            acc = acc + vol[:, s_]
         if cur:
             rounds.append(cur)
         xplan = (rlists, rwords, rounds)
@@ -732,7 +800,7 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
     tp = _phase(prof, "pack", tp)
     met.wire_bytes = int(4 * (lists.sum() + words.sum()) + 16 * P)
     pending = None
-    for rd in rounds:
+    for ri, rd in enumerate(rounds):
         sl, sw = np.zeros(P, np.int64), np.zeros(P, np.int64)
         rl, rw = np.zeros(P, np.int64), np.zeros(P, np.int64)
         if rank in rd:  # this rank's turn: all its messages, grouped by destination
@@ -748,7 +816,7 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
         h_w = yield ("a2a_start", send_w, sw, rw, rpool)
         tp = _phase(prof, "round_setup", tp)
         if pending is not None:  # count the previous round while this one is in flight
-            o, plan = ops.count_received(sh, pending[0], pending[1])
+            o, plan = ops.count_received(sh, pending[0], pending[1], key=(xkey, pending[3]))
             outs.append(o)
             keep.append((plan, pending))
             tp = _phase(prof, "received", tp)
@@ -756,14 +824,18 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 27, met=None, 
         r_ids = yield ("wait", h_w)
         if r_ids.numel() and r_ids.data_ptr() != rpool.data_ptr():
             rpool.copy_(r_ids)
-        pending = (r_len.to(torch.int32).contiguous(), rpool, buf) if int(rl.sum()) else None
+        pending = (r_len.to(torch.int32).contiguous(), rpool, buf, ri) if int(rl.sum()) else None
     tp = _phase(prof, "round_setup", tp)
     if pending is not None:
-        o, plan = ops.count_received(sh, pending[0], pending[1])
+        o, plan = ops.count_received(sh, pending[0], pending[1], key=(xkey, pending[3]))
         outs.append(o)
         keep.append((plan, pending))
         tp = _phase(prof, "received", tp)
     part = ops.finish(outs)
+    rel = getattr(ops, "release_received", None)
+    if rel is not None:
+        for plan, _ in keep:
+            rel(plan)
     del keep
     met.triangles = part
     tot = torch.tensor([part], dtype=torch.int64, device=dev)
@@ -788,7 +860,7 @@ def build_sharded(pairs, pos_base, group=None, cost="predsum", ops=None, keep_ma
     return run_dist(build_gen(pairs, pos_base, P, rank, cost, ops, keep_maps), group)
 
 
-def count_sharded(sh: ShardGraph, group=None, ops=None, round_words=1 << 27):
+def count_sharded(sh: ShardGraph, group=None, ops=None, round_words=1 << 28):
     """The sharded surrogate count on this rank; returns (total, RankMetrics)."""
     import torch.distributed as dist
 
@@ -821,10 +893,15 @@ def emulate_build(raw, P, cost="predsum", ops=None, keep_maps=False, timed=False
     return emulate(gens, timed)
 
 
-def emulate_count(shards, ops=None, round_words=1 << 27, timed=False, profs=None):
+def emulate_count(shards, ops=None, round_words=1 << 28, timed=False, profs=None, busy=None):
     """All P ranks of the sharded count in this process; returns
     (total, [RankMetrics], per-rank device ms)."""
     P = len(shards)
-    res, ms = emulate([count_gen(sh, P, r, ops, round_words, prof=None if profs is None else profs[r])
-                       for r, sh in enumerate(shards)], timed)
+    rops = [ops] * P
+    if busy is not None and ops is None:  # one timed ops object per rank
+        rops = [ShardOps() for _ in range(P)]
+        for o in rops:
+            o.timing = True
+    res, ms = emulate([count_gen(sh, P, r, rops[r], round_words, prof=None if profs is None else profs[r])
+                       for r, sh in enumerate(shards)], timed, busy)
     return res[0][0], [x[1] for x in res], ms

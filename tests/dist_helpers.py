@@ -282,7 +282,7 @@ class NumpyShardOps:
         buf = torch.full((self.HEAD + nw + 4,), self.IMAX, dtype=torch.int32)
         return buf, buf[self.HEAD: self.HEAD + nw]
 
-    def count_received(self, sh, row_len, pool):
+    def count_received(self, sh, row_len, pool, key=None):
         p = self._np(pool)
         rows, off = [], 0
         for d in self._np(row_len).tolist():

@@ -20,7 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg5")
 ap.add_argument("--ranks", default="2,4,8")
 ap.add_argument("--costs", default="predsum,engine")
-ap.add_argument("--round-words", type=int, default=1 << 27)
+ap.add_argument("--round-words", type=int, default=1 << 28)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--rebalance", type=int, default=2, help="measured refinements of the partition after the first count")
 ap.add_argument("--no-prof", action="store_true")
@@ -44,18 +44,22 @@ for cost in a.costs.split(","):
         shards, bms = S.emulate_build(dev_raw, P, cost=cost, timed=True)
         tb = time.perf_counter() - t0
         for it in range(a.rebalance + 1):
-            best = None
+            best, bbusy = None, None
             for _ in range(a.reps):
-                tot, mets, ms = S.emulate_count(shards, round_words=a.round_words, timed=True)
+                busy = [0.0] * P
+                tot, mets, ms = S.emulate_count(shards, round_words=a.round_words, timed=True, busy=busy)
                 assert tot == T, (tot, T)
                 best = ms if best is None else [min(x, y) for x, y in zip(best, ms)]  # per-rank minimum
+                bbusy = busy if bbusy is None else [min(x, y) for x, y in zip(bbusy, busy)]
             res = [sh.resident_bytes() / 2**20 for sh in shards]
             tag = f"cost={cost}" + (f" +{it} measured refinement(s)" if it else "")
             print(f"{a.config} P={P} {tag}: count ranks ms {' '.join(f'{x:.2f}' for x in best)} max {max(best):.2f} "
-                  f"(sum {sum(best):.1f}) -> eff {t1 / (P * max(best)):.2f}; build ranks ms max {max(bms):.1f} (wall {tb:.1f}s); "
+                  f"(sum {sum(best):.1f}) -> eff {t1 / (P * max(best)):.2f}; own kernels ms "
+                  f"{' '.join(f'{x:.2f}' for x in bbusy)} max {max(bbusy):.2f} -> eff {t1 / (P * max(bbusy)):.2f}; "
+                  f"build ranks ms max {max(bms):.1f} (wall {tb:.1f}s); "
                   f"resident MiB max {max(res):.0f}; bounds {shards[0].bounds.tolist()}", flush=True)
             if it < a.rebalance:
-                shards = S.emulate_rebalance(shards, best)
+                shards = S.emulate_rebalance(shards, bbusy)
         if not a.no_prof:
             profs = [dict() for _ in range(P)]
             S.emulate_count(shards, round_words=a.round_words, profs=profs)
