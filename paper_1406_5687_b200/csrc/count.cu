@@ -603,6 +603,81 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
   }
 }
 
+// Block-tier streaming over a row-padded pool (EngineArgs::padded).  Two
+// things the general path pays per window are not needed here:
+//   * id masks: ids of a chunk outside its segment are either <= u (before
+//     the suffix start; every table id is > u) or the row's INT32_MAX
+//     padding, so probing them can never count -- and window lanes past the
+//     group's end read the pool's INT32_MAX head instead of being masked;
+//   * per-window segment resolution (ballot + OR-reduction + two popc + a
+//     16-byte table read): hub suffixes are many chunks long, so each lane
+//     carries its current segment (its end and the address of its flat
+//     chunk 0) from window to window and only steps to the next table entry
+//     when its chunk index passes that end.
+// ncu (cfg 3, profiles/r18_*): resolution + masks were 24 of the 49 warp
+// instructions per window, the probes themselves 20.
+template <int kKind, int kLw, int kCap, class Segs, int kW>
+__device__ __forceinline__ void stream_group_inc(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
+                                                 int g0, int g1, int lane, int& npos, uint32_t& cnt, int4* segtab) {
+  const unsigned FULL = 0xffffffffu;
+  int s = 0, e = 0;
+  if (g0 + lane < g1) segs.get(g0 + lane, s, e);
+  const int len = e - s;
+  const unsigned nz = __ballot_sync(FULL, len > 0);
+  const int nseg = __popc(nz);
+  int src = lane;
+  if (nz & (nz + 1u)) src = (lane < nseg) ? (int)__fns(nz, 0, lane + 1) : 0;
+  const int cs = __shfl_sync(FULL, s, src);
+  int clen = __shfl_sync(FULL, len, src);
+  if (lane >= nseg) clen = 0;
+  const int c0s = cs >> 2;
+  const int nch = (lane < nseg) ? ((cs + clen + 3) >> 2) - c0s : 0;
+  int incl = nch;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(FULL, incl, 31);
+  if (total == 0) return;
+  const int excl = incl - nch;
+  __syncwarp();  // the previous group's reads of segtab are done
+  if (lane < nseg) {
+    const unsigned long long p = (unsigned long long)pool + 16ll * (long long)(c0s - excl);  // flat chunk 0
+    segtab[lane] = make_int4((int)(unsigned)p, (int)(unsigned)(p >> 32), incl, 0);
+  }
+  __syncwarp();
+  const int4* const head = reinterpret_cast<const int4*>(pool) - 1;  // INT32_MAX ids
+  int sj = 0;
+  int4 q = segtab[0];
+  int sEnd = q.z;
+  const int4* sPtr = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
+  int4 v[kW];
+  auto load = [&](int base) {
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+      const int f = base + 32 * k + lane;
+      const int4* p = head;
+      if (f < total) {
+        while (f >= sEnd) {  // segments are non-empty: at most nseg - 1 steps in all
+          q = segtab[++sj];
+          sEnd = q.z;
+          sPtr = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
+        }
+        p = sPtr + f;
+      }
+      v[k] = __ldg(p);
+    }
+  };
+  load(0);
+  for (int base = 0; base < total; base += 32 * kW) {
+#pragma unroll
+    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], 0xFu, lane, npos, cnt);
+    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+    if (base + 32 * kW < total) load(base + 32 * kW);
+  }
+}
+
 struct EngineArgs {
   const int64_t* row_indptr;  // owner -> segment index range
   const int64_t* tab_indptr;  // node -> table list
@@ -1194,7 +1269,7 @@ __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a
 
 // Block tier: owners with d > d_lo (the mid tier's cap).  The block stages the owner's table
 // once per chunk-owner and its 16 warps stream groups of 32 segments.
-template <class Segs>
+template <class Segs, bool kPadded>
 __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(EngineArgs a, Segs segs) {
   extern __shared__ __align__(16) unsigned char big_smem[];
   uint32_t* bm = reinterpret_cast<uint32_t*>(big_smem);
@@ -1291,7 +1366,14 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           // and the wait at the next block barrier is at most one claim long
           const int g = ra + kBigClaim * gi;
           if (g >= rb) break;
-          if (staged_exact)
+          if (kPadded && staged_exact)
+            stream_group_inc<kExact, kLwBig, 1, Segs, kWin>(segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane,
+                                                            npos, acc.cnt, segtab);
+          else if (kPadded)
+            stream_group_inc<kBuckets, kLwBig, TCB_BIG_FB, Segs, kWin>(segs, a.pool, t, g + so,
+                                                                      min(g + kBigClaim, rb) + so, lane, npos, acc.cnt,
+                                                                      segtab);
+          else if (staged_exact)
             // exact tables leave the bucket area free: it holds the warps'
             // cp.async window rings (kBigStages stages of 32 chunks each)
             stream_group<kExact, kLwBig, Segs, 1, kWin, TCB_BIG_SB, TCB_BIG_PIPE, kBigStages>(
@@ -1460,9 +1542,13 @@ static const TierShape& tier_shape() {
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_MID(PullSegs), kMidWarps * 32, 0));
     ts.blocks[1] = std::max(per_sm, 1) * sm_count();
     ts.workers[1] = ts.blocks[1] * kMidWarps;
-    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
-    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PushSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBigSmem));
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine_big<PullSegs>, kBigThreads, kBigSmem));
+    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBigSmem));
+    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBigSmem));
+    TC_CUDA(cudaFuncSetAttribute(k_engine_big<PushSegs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBigSmem));
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_engine_big<PullSegs, true>, kBigThreads, kBigSmem));
     ts.blocks[2] = std::max(per_sm, 1) * sm_count();
 #ifndef TCB_BIG_WORKERS_X4
 #define TCB_BIG_WORKERS_X4 8
@@ -1724,7 +1810,8 @@ static void launch_tier(EngineLaunch& L, int k, Segs segs, cudaStream_t s, const
   } else if (k == 1) {
     K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
   } else {
-    k_engine_big<Segs><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
+    if (L.args[2].padded) k_engine_big<Segs, true><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
+    else k_engine_big<Segs, false><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
   }
   check_launch();
 }

@@ -344,6 +344,35 @@ def test_engine_tiers_forced(caps):
         L.tc_set_tuning(1, -1)
 
 
+def test_block_tier_hashed_tables_wide_spans():
+    """Owners whose table ids span more than the block tier's exact bitmap
+    (2^18 ids) take its hashed filter + bucket tables; with the warp caps
+    lowered every owner of a sparse 1 M-node uniform graph streams through
+    the block tier's padded-pool path (incremental segment resolution, no id
+    masks).  Checked against the oracle, both engines, and the partials."""
+    from paper_1406_5687_b200 import _lib
+    L = _lib.lib()
+    raw = er_edges(1_000_000, 9_000_000, 17)
+    og = O.build_graph(*O.normalize(raw.cpu().numpy().astype(np.int64)))
+    T = O.count_triangles(og)
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph(n=0, edges=raw)))
+    span = og.eff_indices[og.eff_indptr[1:][og.eff_deg > 4] - 1] - og.eff_indices[og.eff_indptr[:-1][og.eff_deg > 4]]
+    assert int(span.max()) > (1 << 18)
+    try:
+        for caps in ((2, 4, 4096), (0, 0, 4096), (0, 0, 4)):
+            _lib.check(L.tc_set_tuning(0, caps[0]))
+            _lib.check(L.tc_set_tuning(2, caps[1]))
+            _lib.check(L.tc_set_tuning(1, caps[2]))
+            assert tcb.count_triangles_seq(g) == T, caps
+            assert int(count_lowest(g).item()) == T, caps
+            b = torch.as_tensor(O.balanced_bounds(O.node_costs(og, "predsum"), 0, og.n, 5)).cuda()
+            assert int(count_middle(g, 0, g.n, bounds=b).sum()) == T, caps
+    finally:
+        L.tc_set_tuning(0, -1)
+        L.tc_set_tuning(2, -1)
+        L.tc_set_tuning(1, -1)
+
+
 def test_dense_core_block_tier():
     """A dense core (K_320 plus random edges) puts d^ > 256 tables on the
     block tier at default caps; checked against the oracle."""
