@@ -510,10 +510,13 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
     rebal_ms = []
     for it in range(refinements + 1):
         timed_counts(warmup)
+        ts, T, met = timed_counts(steps)
+        # the rank's own device work, for the refinement: measurement mode runs
+        # a count on one stream with its kernels bracketed by events
         ops.timing = True
         ops.busy_ms()
-        ts, T, met = timed_counts(steps)
-        busy = ops.busy_ms() / steps
+        timed_counts(2)
+        busy = ops.busy_ms() / 2
         ops.timing = False
         trail.append({"count_ms": max_over_ranks(statistics.median(ts)), "rank_busy_ms_max": max_over_ranks(busy),
                       "bounds": [int(x) for x in sh.bounds]})

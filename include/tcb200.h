@@ -457,18 +457,20 @@ int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nr
  * row after each u (surrogate_count_list, _kernels.py:70-80), grouped by
  * owner -- rev_indptr int64[hi-lo+1], rev_seg int32[2*cap], rev_cost
  * int64[hi-lo+1] (tables tab_indptr indexed u - lo) for tc_plan_middle with
- * pool_padded = 1.  cap >= the number of row entries.  nseg_host (nullable)
- * synchronises. */
-int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
-                   const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr, int32_t* rev_seg,
-                   int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream);
+ * pool_padded = 1.  cap >= the number of row entries; pool_words = the ids
+ * the rows occupy (a launch-shape hint: short rows get 8 lanes each; 0 =
+ * unknown).  nseg_host (nullable) synchronises. */
+int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t pool_words, int64_t lo,
+                   int64_t hi, const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr,
+                   int32_t* rev_seg, int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream);
 
 /* The scatter pass of tc_shard_index for rows whose per-owner offsets
  * rev_indptr are kept from an earlier call on lists of the same structure
  * (the same exchange round of the same partitioned graph): fills
  * pool_indptr and rev_seg only. */
-int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
-                        const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg, tc_stream_t stream);
+int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t pool_words, int64_t lo,
+                        int64_t hi, const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg,
+                        tc_stream_t stream);
 
 /* ------------------------------------------------------------ NCCL layer */
 

@@ -75,8 +75,8 @@ _SIGS = {
     "tc_shard_send_plan_len": [_i64, _i32, _pi64],
     "tc_shard_send_sizes": [_vp, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp],
     "tc_shard_send_pack": [_vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp],
-    "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
-    "tc_shard_index_emit": [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp],
+    "tc_shard_index": [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
+    "tc_shard_index_emit": [_vp, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "tc_nccl_unique_id": [_vp],
     "tc_nccl_init_rank": [_vp, _i32, _i32, ctypes.POINTER(_vp)],
     "tc_nccl_init_all": [_i32, _vp, _vp],

@@ -47,6 +47,12 @@
 
 namespace tcb {
 
+#ifndef TCB_MID_PAD_MODE
+#define TCB_MID_PAD_MODE 2  // padded pools in the mid tier: 0 id masks as for any pool, 2 no masks
+#endif
+#ifndef TCB_BIG_INC_PIPE
+#define TCB_BIG_INC_PIPE 0
+#endif
 #ifndef TCB_MINBLOCKS
 #define TCB_MINBLOCKS 5
 #endif
@@ -115,7 +121,12 @@ static constexpr int kBigCap = TCB_BIG_CAP;  // block tier: ids per staged table
 static constexpr int kLwBig = 13;         // block tier filter: 2^13 words = 256K bits (32 KB)
 static constexpr int kLbBig = TCB_BIG_LB;  // block tier buckets: 2^11 x 4 ids (32 KB), load <= 1/2
 static constexpr int kPosCap = TCB_POS_CAP;  // block tier: per-warp queue of filter hits
-static constexpr int kPosDrain = kPosCap - 128 * TCB_WINDOWS;  // drain before a step could overflow
+#ifndef TCB_BIG_WINDOWS
+#define TCB_BIG_WINDOWS 3  // block tier: windows in flight per warp (2 -> 3: cfg 4 block tier 114.0 -> 106.4 ms)
+#endif
+static constexpr int kBigWin = TCB_BIG_WINDOWS;
+static constexpr int kPosDrain = kPosCap - 128 * kBigWin;  // drain before a step could overflow
+static_assert(kPosDrain > 0, "the block tier's hit queue must hold one step of hits");
 #ifndef TCB_SBWORDS
 #define TCB_SBWORDS 64
 #endif
@@ -345,7 +356,7 @@ __device__ __forceinline__ void probe4(const Table& t, int4 v, uint32_t vmask, i
 // count << 2).
 // Resolves and loads the kW windows starting at chunk `base` (see
 // probe_group).
-template <int kW, bool kMayFast>
+template <int kW, bool kMayFast, bool kNoMask = false>
 __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, bool lane_seg, int excl,
                                              const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
                                              int total, int lane, bool fast_rt, int base, int& cbase, int4 (&v)[kW],
@@ -383,8 +394,10 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
         v[k] = __ldg(&pool4[q.x + f]);
 #endif
         uint32_t mk = 0xFu;
-        if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
-        if (f == (q.w >> 8)) mk &= ((uint32_t)q.w >> 4) & 0xFu;
+        if (!kNoMask) {  // row-padded pools need no id masks (see stream_group_inc)
+          if (f == q.z) mk &= (uint32_t)q.w & 0xFu;
+          if (f == (q.w >> 8)) mk &= ((uint32_t)q.w >> 4) & 0xFu;
+        }
         vm[k] = mk;
       }
     }
@@ -401,7 +414,7 @@ __device__ __forceinline__ void load_windows(const int4* __restrict__ pool4, boo
 // 2 kW loads per warp are in flight across the probe work.  Measured: the
 // mid tier gains (cfg 5 24.2 -> 20.6 ms), the small tier loses (cfg 2 2.49 ->
 // 2.61 ms: registers), so only the mid tier pipelines.
-template <int kKind, int kLw, int kCap, int kW, bool kFast, bool kPipe>
+template <int kKind, int kLw, int kCap, int kW, bool kFast, bool kPipe, bool kNoMask = false>
 __device__ __forceinline__ void probe_loop(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                            const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
                                            int total, int lane, int& npos, uint32_t& cnt, bool fast = kFast) {
@@ -409,14 +422,14 @@ __device__ __forceinline__ void probe_loop(const int4* __restrict__ pool4, const
   int cbase = 0;  // fast path: segments starting before the window
   int4 v[kW];
   uint32_t vm[kW];
-  load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, 0, cbase, v, vm);
+  load_windows<kW, kFast, kNoMask>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, 0, cbase, v, vm);
   for (int base = 0; base < total; base += 32 * kW) {
     if (kPipe) {
       int4 nv[kW];
       uint32_t nvm[kW];
       const int nb = base + 32 * kW;
       if (nb < total) {
-        load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, nb, cbase, nv, nvm);
+        load_windows<kW, kFast, kNoMask>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, nb, cbase, nv, nvm);
       } else {
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
@@ -437,7 +450,7 @@ __device__ __forceinline__ void probe_loop(const int4* __restrict__ pool4, const
       for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], vm[k], lane, npos, cnt);
       if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
       if (base + 32 * kW < total)
-        load_windows<kW, kFast>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, base + 32 * kW, cbase, v,
+        load_windows<kW, kFast, kNoMask>(pool4, lane_seg, excl, segtab, sbits, total, lane, fast, base + 32 * kW, cbase, v,
                                  vm);
     }
   }
@@ -523,7 +536,7 @@ __device__ __forceinline__ void probe_loop_async(const Table& t, int nseg, int e
 // kSbW: words of the warp's start bitmap (groups of <= 32 kSbW chunks take
 // the bitmap path).
 template <int kKind, int kLw, int kCap = 1, int kW = kWin, bool kSb = true, bool kPipe = false, int kS = 0,
-          int kSbW = kSbWords>
+          int kSbW = kSbWords, bool kNoMask = false>
 __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, const Table& t, int nseg, int excl,
                                             const int4* __restrict__ segtab, const uint32_t* __restrict__ sbits,
                                             int total, int lane, int& npos, uint32_t& cnt, int4* ring = nullptr) {
@@ -533,7 +546,8 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
                                                               fast, ring);
     return;
   }
-  probe_loop<kKind, kLw, kCap, kW, kSb, kPipe>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt, fast);
+  probe_loop<kKind, kLw, kCap, kW, kSb, kPipe, kNoMask>(pool4, t, nseg, excl, segtab, sbits, total, lane, npos, cnt,
+                                                       fast);
 }
 
 // One warp streams segments [g0, g1) (g1 - g0 <= 32) of the current owner;
@@ -542,7 +556,7 @@ __device__ __forceinline__ void probe_group(const int4* __restrict__ pool4, cons
 // kSb: use the start bitmap (warp tiers; hub groups of the block tier are
 // mostly longer than 1024 chunks and keep the ballot/redux resolution).
 template <int kKind, int kLw, class Segs, int kCap = 1, int kW = kWin, bool kSb = true, bool kPipe = false,
-          int kS = 0, int kSbW = kSbWords>
+          int kS = 0, int kSbW = kSbWords, bool kNoMask = false>
 __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                              int g0, int g1, int lane, int& npos, uint32_t& cnt,
                                              int4* segtab, int pf_end = 0, int4* ring = nullptr) {
@@ -595,8 +609,8 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
 #if TCB_PF_NEXT
   for (int c = s2 & ~31; c < e2; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(pool + c));
 #endif
-  probe_group<kKind, kLw, kCap, kW, kSb, kPipe, kS, kSbW>(reinterpret_cast<const int4*>(pool), t, nseg, excl, segtab,
-                                                    sbits, total, lane, npos, cnt, ring);
+  probe_group<kKind, kLw, kCap, kW, kSb, kPipe, kS, kSbW, kNoMask>(reinterpret_cast<const int4*>(pool), t, nseg, excl,
+                                                             segtab, sbits, total, lane, npos, cnt, ring);
   if (fast) {
     __syncwarp();
     if (lane < nseg) sbits[excl >> 5] = 0;
@@ -671,10 +685,20 @@ __device__ __forceinline__ void stream_group_inc(const Segs& segs, const int32_t
   };
   load(0);
   for (int base = 0; base < total; base += 32 * kW) {
+#if TCB_BIG_INC_PIPE
+    int4 cur[kW];
+#pragma unroll
+    for (int k = 0; k < kW; ++k) cur[k] = v[k];
+    if (base + 32 * kW < total) load(base + 32 * kW);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, cur[k], 0xFu, lane, npos, cnt);
+    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+#else
 #pragma unroll
     for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], 0xFu, lane, npos, cnt);
     if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
     if (base + 32 * kW < total) load(base + 32 * kW);
+#endif
   }
 }
 
@@ -823,7 +847,7 @@ struct Acc {
 // Warp tiers (small: d <= 256 in 3 KB slices, 8 warps/block; mid:
 // d <= 1024 in 8 KB slices, 4 warps/block): each warp owns a private slice.
 template <class Segs, int kLb, int kLw, int kWPB, int kMinB, int kW, bool kPipe, int kS = 0, int kSbW = kSbWords,
-          int kFb = 1>
+          int kFb = 1, bool kPadded = false>
 __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs segs) {
   __shared__ WarpSliceT<kLb, kLw> slices[kWPB];
   __shared__ int4 segtabs[kWPB][32 + kSbW / 4];
@@ -880,8 +904,14 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
         Table t{sl.bm, nullptr, nullptr, nullptr, d, 0, tlo, 0, 0, span};
         int npos = 0;
         for (int g = ra; g < rb; g += 32)
-          stream_group<kExact, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
-                                                                        lane, npos, acc.cnt, segtab, rb + so, ring);
+          if (kPadded && TCB_MID_PAD_MODE == 2)
+            stream_group<kExact, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW, true>(segs, a.pool, t, g + so,
+                                                                                min(g + 32, rb) + so, lane, npos,
+                                                                                acc.cnt, segtab, rb + so, ring);
+          else
+            stream_group<kExact, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so,
+                                                                          min(g + 32, rb) + so, lane, npos, acc.cnt,
+                                                                          segtab, rb + so, ring);
         __syncwarp();
 #if TCB_WIPE
         wipe_filter<kLw + 0>(sl.bm, lane, kExactWords);
@@ -905,8 +935,14 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
       __syncwarp();
       int npos = 0;
       for (int g = ra; g < rb; g += 32)
-        stream_group<kInline, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so, min(g + 32, rb) + so,
-                                                                       lane, npos, acc.cnt, segtab, rb + so, ring);
+        if (kPadded && TCB_MID_PAD_MODE == 2)
+          stream_group<kInline, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW, true>(segs, a.pool, t, g + so,
+                                                                               min(g + 32, rb) + so, lane, npos,
+                                                                               acc.cnt, segtab, rb + so, ring);
+        else
+          stream_group<kInline, kLw, Segs, kFb, kW, true, kPipe, kS, kSbW>(segs, a.pool, t, g + so,
+                                                                         min(g + 32, rb) + so, lane, npos, acc.cnt,
+                                                                         segtab, rb + so, ring);
       __syncwarp();
 #if TCB_WIPE
       wipe_filter<kLw>(sl.bm, lane);
@@ -1367,20 +1403,20 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           const int g = ra + kBigClaim * gi;
           if (g >= rb) break;
           if (kPadded && staged_exact)
-            stream_group_inc<kExact, kLwBig, 1, Segs, kWin>(segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane,
+            stream_group_inc<kExact, kLwBig, 1, Segs, kBigWin>(segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane,
                                                             npos, acc.cnt, segtab);
           else if (kPadded)
-            stream_group_inc<kBuckets, kLwBig, TCB_BIG_FB, Segs, kWin>(segs, a.pool, t, g + so,
+            stream_group_inc<kBuckets, kLwBig, TCB_BIG_FB, Segs, kBigWin>(segs, a.pool, t, g + so,
                                                                       min(g + kBigClaim, rb) + so, lane, npos, acc.cnt,
                                                                       segtab);
           else if (staged_exact)
             // exact tables leave the bucket area free: it holds the warps'
             // cp.async window rings (kBigStages stages of 32 chunks each)
-            stream_group<kExact, kLwBig, Segs, 1, kWin, TCB_BIG_SB, TCB_BIG_PIPE, kBigStages>(
+            stream_group<kExact, kLwBig, Segs, 1, kBigWin, TCB_BIG_SB, TCB_BIG_PIPE, kBigStages>(
                 segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab, 0,
                 bkt + warp * (kBigStages > 0 ? kBigStages * 32 : 0));
           else
-            stream_group<kBuckets, kLwBig, Segs, TCB_BIG_FB, kWin, TCB_BIG_SB, TCB_BIG_PIPE>(
+            stream_group<kBuckets, kLwBig, Segs, TCB_BIG_FB, kBigWin, TCB_BIG_SB, TCB_BIG_PIPE>(
                 segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
         }
         if (!staged_exact) drain(t, npos, lane, acc.cnt);
@@ -1388,7 +1424,7 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
         Table t{nullptr, gtab, nullptr, nullptr, d, 0, __ldg(&gtab[0]), __ldg(&gtab[d - 1]), 0, 0};
         int npos = 0;
         for (int g = ra + 32 * warp; g < rb; g += 32 * nwarps)
-          stream_group<kGlobal, 0, Segs, 1, kWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
+          stream_group<kGlobal, 0, Segs, 1, kBigWin, false, TCB_BIG_PIPE>(segs, a.pool, t, g + so, min(g + 32, rb) + so, lane, npos,
                                    acc.cnt, segtab);
       }
     }
@@ -1521,6 +1557,8 @@ static long long g_engine_launches = 0;
 #endif
 #define K_MID(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE, TCB_MID_STAGES, \
                           TCB_MID_SBW, TCB_MID_FB>
+#define K_MID_PAD(S) k_engine<S, kLbMid, kLwMid, kMidWarps, TCB_MID_MINB, TCB_MID_WINDOWS, TCB_MID_PIPE, \
+                              TCB_MID_STAGES, TCB_MID_SBW, TCB_MID_FB, true>
 
 struct TierShape {
   int blocks[3];   // persistent grid per tier
@@ -1539,7 +1577,7 @@ static const TierShape& tier_shape() {
 #endif
     ts.blocks[0] = std::max(per_sm, 1) * sm_count();
     ts.workers[0] = ts.blocks[0] * kWarps;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_MID(PullSegs), kMidWarps * 32, 0));
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_MID_PAD(PullSegs), kMidWarps * 32, 0));
     ts.blocks[1] = std::max(per_sm, 1) * sm_count();
     ts.workers[1] = ts.blocks[1] * kMidWarps;
     TC_CUDA(cudaFuncSetAttribute(k_engine_big<PullSegs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1808,7 +1846,8 @@ static void launch_tier(EngineLaunch& L, int k, Segs segs, cudaStream_t s, const
     K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
 #endif
   } else if (k == 1) {
-    K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
+    if (L.args[1].padded) K_MID_PAD(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
+    else K_MID(Segs)<<<ts.blocks[1], kMidWarps * 32, 0, s>>>(L.args[1], segs);
   } else {
     if (L.args[2].padded) k_engine_big<Segs, true><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);
     else k_engine_big<Segs, false><<<ts.blocks[2], kBigThreads, kBigSmem, s>>>(L.args[2], segs);

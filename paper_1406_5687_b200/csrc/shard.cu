@@ -482,18 +482,20 @@ __global__ void __launch_bounds__(kBlk) k_sh_send_emit(const int64_t* __restrict
 // and their total length in one 64-bit atomic (count << 40 | length sum);
 // pass 2 scatters the segments with a 32-bit cursor.
 static constexpr int kCntShift = 40;
+// kG lanes per row (8 for short lists, 32 otherwise): a lane walks ids
+// jl, jl + kG, ... of its row and stops at the first id >= hi (rows ascend,
+// so its later ids are not owned either).
+template <int kG>
 __global__ void k_sh_idx_count(const int64_t* __restrict__ pptr, const int32_t* __restrict__ len, int64_t nrow,
                                const int32_t* __restrict__ pool, int64_t lo, int64_t hi, unsigned long long* acc) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
+  const int jl = threadIdx.x % kG;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / kG;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG; r < nrow; r += ng) {
     const int64_t p = pptr[r], d = len[r];
-    for (int64_t b = 0; b + 1 < d; b += 32) {  // rows ascend: stop after the owned ids
-      const int64_t i = b + lane;
-      const int32_t u = (i + 1 < d) ? pool[p + i] : INT32_MAX;
-      if (u >= lo && u < hi)
-        atomicAdd(&acc[u - lo], (1ull << kCntShift) + (unsigned long long)(d - i - 1));
-      if (__all_sync(0xffffffffu, u >= hi)) break;
+    for (int64_t i = jl; i + 1 < d; i += kG) {
+      const int32_t u = pool[p + i];
+      if (u >= hi) break;
+      if (u >= lo) atomicAdd(&acc[u - lo], (1ull << kCntShift) + (unsigned long long)(d - i - 1));
     }
   }
 }
@@ -522,18 +524,18 @@ __global__ void k_sh_idx_cursor(const int64_t* __restrict__ rev_indptr, int64_t 
   GRID_STRIDE(x, nx) cursor[x] = (int32_t)rev_indptr[x];
 }
 
+template <int kG>
 __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* __restrict__ len, int64_t nrow,
                               const int32_t* __restrict__ pool, int64_t lo, int64_t hi,
                               const int64_t* __restrict__ rev_indptr, int32_t* cursor, int2* rev_seg) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrow; r += nw) {
+  const int jl = threadIdx.x % kG;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / kG;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kG; r < nrow; r += ng) {
     const int64_t p = pptr[r], d = len[r];
-    for (int64_t b = 0; b + 1 < d; b += 32) {
-      const int64_t i = b + lane;
-      const int32_t u = (i + 1 < d) ? pool[p + i] : INT32_MAX;
-      if (__all_sync(0xffffffffu, u >= hi)) break;
-      if (u >= lo && u < hi) {
+    for (int64_t i = jl; i + 1 < d; i += kG) {
+      const int32_t u = pool[p + i];
+      if (u >= hi) break;
+      if (u >= lo) {
         const int64_t x = u - lo;
         const int64_t slot = atomicAdd(&cursor[x], 1);
 #if TCB_DEBUG
@@ -543,6 +545,12 @@ __global__ void k_sh_idx_emit(const int64_t* __restrict__ pptr, const int32_t* _
       }
     }
   }
+}
+
+// lanes per row of the receive-index kernels for rows of this mean padded
+// length (pool_words 0: unknown)
+static int idx_group(int64_t nrow, int64_t pool_words) {
+  return (nrow > 0 && pool_words > 0 && pool_words / nrow < 96) ? 8 : 32;
 }
 
 }  // namespace tcb
@@ -886,9 +894,9 @@ int tc_shard_send_pack(const int64_t* indptr, const int32_t* indices, int64_t nr
   });
 }
 
-int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
-                   const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr, int32_t* rev_seg,
-                   int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream) {
+int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t pool_words, int64_t lo,
+                   int64_t hi, const int64_t* tab_indptr, int64_t* pool_indptr, int64_t* rev_indptr,
+                   int32_t* rev_seg, int64_t* rev_cost, int64_t* nseg_host, tc_stream_t stream) {
   return guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
     TC_REQUIRE(lo >= 0 && lo <= hi, TC_EINVAL, "bad owner range");
@@ -901,9 +909,11 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
     ex_sum(sc, sz, pool_indptr, nrow + 1, s);
     auto* acc = sc.alloc<unsigned long long>(nx + 1);
     TC_CUDA(cudaMemsetAsync(acc, 0, (nx + 1) * sizeof(unsigned long long), s));
-    const int grid = grid_for(std::max<int64_t>(nrow, 1) * 32, kBlk, sm_count() * 16);
+    const int G = idx_group(nrow, pool_words);
+    const int grid = grid_for(std::max<int64_t>(nrow, 1) * G, kBlk, sm_count() * 16);
     if (nrow > 0) {
-      k_sh_idx_count<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, acc);
+      if (G == 8) k_sh_idx_count<8><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, acc);
+      else k_sh_idx_count<32><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, acc);
       check_launch();
     }
     int64_t* cnt = sc.alloc<int64_t>(nx + 1);
@@ -916,8 +926,12 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
     k_sh_idx_cursor<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(rev_indptr, nx, cur);
     check_launch();
     if (nrow > 0) {
-      k_sh_idx_emit<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
-                                          reinterpret_cast<int2*>(rev_seg));
+      if (G == 8)
+        k_sh_idx_emit<8><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
+                                               reinterpret_cast<int2*>(rev_seg));
+      else
+        k_sh_idx_emit<32><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
+                                                reinterpret_cast<int2*>(rev_seg));
       check_launch();
     }
     if (nseg_host) *nseg_host = scalar_of(rev_indptr + nx, s);
@@ -929,8 +943,9 @@ int tc_shard_index(const int32_t* row_len, int64_t nrow, const int32_t* pool, in
 // lists at every count of a partitioned graph, so the per-owner counts, the
 // cost prefix and the engine plan built from them are kept and only the
 // segments are scattered again.
-int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t lo, int64_t hi,
-                        const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg, tc_stream_t stream) {
+int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* pool, int64_t pool_words, int64_t lo,
+                        int64_t hi, const int64_t* rev_indptr, int64_t* pool_indptr, int32_t* rev_seg,
+                        tc_stream_t stream) {
   return guarded([&] {
     cudaStream_t s = (cudaStream_t)stream;
     TC_REQUIRE(lo >= 0 && lo <= hi, TC_EINVAL, "bad owner range");
@@ -944,9 +959,14 @@ int tc_shard_index_emit(const int32_t* row_len, int64_t nrow, const int32_t* poo
     k_sh_idx_cursor<<<grid_for(nx + 1, kBlk), kBlk, 0, s>>>(rev_indptr, nx, cur);
     check_launch();
     if (nrow > 0) {
-      const int grid = grid_for(nrow * 32, kBlk, sm_count() * 16);
-      k_sh_idx_emit<<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
-                                          reinterpret_cast<int2*>(rev_seg));
+      const int G = idx_group(nrow, pool_words);
+      const int grid = grid_for(nrow * G, kBlk, sm_count() * 16);
+      if (G == 8)
+        k_sh_idx_emit<8><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
+                                               reinterpret_cast<int2*>(rev_seg));
+      else
+        k_sh_idx_emit<32><<<grid, kBlk, 0, s>>>(pool_indptr, row_len, nrow, pool, lo, hi, rev_indptr, cur,
+                                                reinterpret_cast<int2*>(rev_seg));
       check_launch();
     }
   });

@@ -122,16 +122,22 @@ class ShardOps:
         e.record(stream or torch.cuda.current_stream(self.dev))
         return e
 
-    def _toc(self, e0, stream=None):
+    def _toc(self, e0, stream=None, label="engine"):
         if e0 is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(stream or torch.cuda.current_stream(self.dev))
-            self._busy.append((e0, e1))
+            self._busy.append((e0, e1, label))
 
-    def busy_ms(self):
-        """Device time of the bracketed work since the last call."""
+    def busy_ms(self, by_label=None):
+        """Device time of the bracketed work since the last call (by_label:
+        a dict that receives the split into pack / index / engine)."""
         torch.cuda.synchronize(self.dev)
-        t = sum(a.elapsed_time(b) for a, b in self._busy)
+        t = 0.0
+        for a, b, label in self._busy:
+            dt = a.elapsed_time(b)
+            t += dt
+            if by_label is not None:
+                by_label[label] = by_label.get(label, 0.0) + dt
         self._busy = []
         return t
 
@@ -267,7 +273,7 @@ class ShardOps:
         self.L.call("tc_shard_send_pack", self.L.ptr(sh.indptr), self.L.ptr(sh.indices), sh.hi - sh.lo,
                     self.L.ptr(sh.pool_indptr), self.L.ptr(sh.pool), self.L.ptr(sh.cache["bounds_dev"]), int(P),
                     int(rank), self.L.ptr(sizes_dev), self.L.ptr(lens), self.L.ptr(ids), self.L.stream())
-        self._toc(t0)
+        self._toc(t0, label="pack")
         return lens[:nl], ids[:nw]
 
     def recv_pool(self, nw):
@@ -284,6 +290,11 @@ class ShardOps:
             st = self._st = (torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev),
                              torch.cuda.Stream(device=self.dev))
             self._turn = 0
+        if self.timing:
+            # measurement mode: everything on the current stream, so the event
+            # brackets do not overlap and their sum is the rank's device work
+            cur = torch.cuda.current_stream(self.dev)
+            return (cur, cur, cur)
         return st
 
     def _plan(self, sh, row_len, pool):
@@ -297,7 +308,8 @@ class ShardOps:
         cap = max(int(pool.numel()), 1)
         rseg = torch.empty(2 * cap, dtype=torch.int32, device=self.dev)
         rcost = torch.empty(nx + 1, dtype=torch.int64, device=self.dev)
-        L.call("tc_shard_index", L.ptr(row_len), nrow, L.ptr(pool), sh.lo, sh.hi, L.ptr(sh.indptr), L.ptr(pip),
+        L.call("tc_shard_index", L.ptr(row_len), nrow, L.ptr(pool), int(pool.numel()), sh.lo, sh.hi, L.ptr(sh.indptr),
+               L.ptr(pip),
                L.ptr(rip), L.ptr(rseg), L.ptr(rcost), None, L.stream())
         h = ctypes.c_void_p()
         L.call("tc_plan_middle", L.ptr(sh.indptr), L.ptr(sh.indices), L.ptr(rip), L.ptr(rseg), L.ptr(rcost),
@@ -358,12 +370,13 @@ class ShardOps:
                 pip = torch.empty(nrow + 1, dtype=torch.int64, device=self.dev)
                 rseg = torch.empty(2 * max(int(pool.numel()), 1), dtype=torch.int32, device=self.dev)
                 rip = plan.keep[1]
-                L.call("tc_shard_index_emit", L.ptr(row_len), nrow, L.ptr(pool), sh.lo, sh.hi, L.ptr(rip), L.ptr(pip),
+                L.call("tc_shard_index_emit", L.ptr(row_len), nrow, L.ptr(pool), int(pool.numel()), sh.lo, sh.hi, L.ptr(rip),
+                       L.ptr(pip),
                        L.ptr(rseg), L.stream())
                 L.call("tc_plan_rebind", plan.handle, L.ptr(rseg), L.ptr(pool))
                 # the plan's handle keeps the offsets and costs; this count's arrays live until finish
                 plan.keep = (pip, rip, rseg, plan.keep[3], pool, row_len)
-            self._toc(t0, plan_s)
+            self._toc(t0, plan_s, "index")
         return self._launch(plan), plan
 
     def release_received(self, plan):
@@ -513,7 +526,7 @@ def run_capi(gen, comm: CComm):
             raise ValueError(f"unknown collective {kind}")
 
 
-def emulate(gens, timed=False, busy=None):
+def emulate(gens, timed=False, busy=None, labels=None):
     """Runs P rank generators in lockstep in this process (one device): every
     collective is performed once all ranks have reached it.  With timed=True
     each rank's device work between collectives is bracketed by CUDA events
@@ -545,7 +558,11 @@ def emulate(gens, timed=False, busy=None):
                 done[r] = True
                 out[r] = stop.value
             if o is not None and getattr(o, "timing", False):
-                busy[r] += o.busy_ms()
+                lab = {}
+                busy[r] += o.busy_ms(lab)
+                if labels is not None:
+                    for k, v in lab.items():
+                        labels[r][k] = labels[r].get(k, 0.0) + v
             if timed:
                 # the segment's side-stream work (engine runs, planning) is
                 # counted with it: per-rank time is serialised (no overlap
@@ -893,15 +910,17 @@ def emulate_build(raw, P, cost="predsum", ops=None, keep_maps=False, timed=False
     return emulate(gens, timed)
 
 
-def emulate_count(shards, ops=None, round_words=1 << 28, timed=False, profs=None, busy=None):
+def emulate_count(shards, ops=None, round_words=1 << 28, timed=False, profs=None, busy=None, labels=None):
     """All P ranks of the sharded count in this process; returns
     (total, [RankMetrics], per-rank device ms)."""
     P = len(shards)
-    rops = [ops] * P
+    rops = list(ops) if isinstance(ops, (list, tuple)) else [ops] * P  # one ops object per rank, or a shared one
     if busy is not None and ops is None:  # one timed ops object per rank
         rops = [ShardOps() for _ in range(P)]
+    if busy is not None:
         for o in rops:
-            o.timing = True
+            if hasattr(o, "busy_ms"):
+                o.timing = True
     res, ms = emulate([count_gen(sh, P, r, rops[r], round_words, prof=None if profs is None else profs[r])
-                       for r, sh in enumerate(shards)], timed, busy)
+                       for r, sh in enumerate(shards)], timed, busy, labels)
     return res[0][0], [x[1] for x in res], ms

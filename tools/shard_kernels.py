@@ -16,12 +16,22 @@ ap.add_argument("--config", default="cfg5")
 ap.add_argument("--ranks", type=int, default=8)
 ap.add_argument("--cost", default="engine")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--rebalance", type=int, default=0)
 a = ap.parse_args()
 raw = bench.host_raw_edges(a.config, pin=True).cuda()
 shards, _ = S.emulate_build(raw, a.ranks, cost=a.cost)
 del raw
 for _ in range(2):
     S.emulate_count(shards)
+for it in range(a.rebalance):
+    busy = [0.0] * a.ranks
+    S.emulate_count(shards, busy=busy)
+    print(f"refinement {it}: own kernels ms {' '.join(f'{x:.2f}' for x in busy)}; bounds {shards[0].bounds.tolist()}")
+    shards = S.emulate_rebalance(shards, busy)
+    S.emulate_count(shards)
+busy = [0.0] * a.ranks
+S.emulate_count(shards, busy=busy)
+print(f"profiled partition: own kernels ms {' '.join(f'{x:.2f}' for x in busy)}; bounds {shards[0].bounds.tolist()}")
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(a.reps):

@@ -43,11 +43,12 @@ for cost in a.costs.split(","):
         t0 = time.perf_counter()
         shards, bms = S.emulate_build(dev_raw, P, cost=cost, timed=True)
         tb = time.perf_counter() - t0
+        rops = [S.ShardOps() for _ in range(P)]  # one per emulated rank, kept across counts (streams, allocator pools)
         for it in range(a.rebalance + 1):
             best, bbusy = None, None
             for _ in range(a.reps):
                 busy = [0.0] * P
-                tot, mets, ms = S.emulate_count(shards, round_words=a.round_words, timed=True, busy=busy)
+                tot, mets, ms = S.emulate_count(shards, ops=rops, round_words=a.round_words, timed=True, busy=busy)
                 assert tot == T, (tot, T)
                 best = ms if best is None else [min(x, y) for x, y in zip(best, ms)]  # per-rank minimum
                 bbusy = busy if bbusy is None else [min(x, y) for x, y in zip(bbusy, busy)]
@@ -58,6 +59,9 @@ for cost in a.costs.split(","):
                   f"{' '.join(f'{x:.2f}' for x in bbusy)} max {max(bbusy):.2f} -> eff {t1 / (P * max(bbusy)):.2f}; "
                   f"build ranks ms max {max(bms):.1f} (wall {tb:.1f}s); "
                   f"resident MiB max {max(res):.0f}; bounds {shards[0].bounds.tolist()}", flush=True)
+            labels = [dict() for _ in range(P)]
+            S.emulate_count(shards, ops=rops, round_words=a.round_words, timed=True, busy=[0.0] * P, labels=labels)
+            print("      split " + " | ".join(" ".join(f"{k[0]}{v:.1f}" for k, v in sorted(lb.items())) for lb in labels), flush=True)
             if it < a.rebalance:
                 shards = S.emulate_rebalance(shards, bbusy)
         if not a.no_prof:
