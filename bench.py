@@ -476,6 +476,7 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
     m_raw = int(raw.shape[0])
     sl, base = S.slice_of(raw, world, rank)
     sl = sl.contiguous().clone()
+    sl_dev = sl.device
     del raw
     torch.cuda.empty_cache()
     builds = []
@@ -530,6 +531,13 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
             rebal_ms.append(max_over_ranks(s.elapsed_time(e)))
             timed_counts(1)
     ms = trail[-1]["count_ms"]
+    # per-rank rows of the reference's run CSV (metrics.py:49-116) from this run
+    import io
+
+    from paper_1406_5687_b200.metrics import write_run_csv
+    mets = S.gather_metrics(met, busy_ms=busy, device=sl_dev)
+    fh = io.StringIO()
+    write_run_csv([S.run_record(T, mets, ms / 1e3, graph=cfg, seed=CONFIGS[cfg].get("seed", 0), cost=cost)], fh)
     bms = max_over_ranks(min(builds))
     res = max_over_ranks(float(sh.resident_bytes()))
     want, src = golden_T(cfg)
@@ -538,7 +546,7 @@ def partitioned_config(cfg, steps, warmup, cost, max_over_ranks, barrier, round_
            "triangles_golden": want, "triangles_ok": (want == T) if want is not None else None, "count_ms": ms,
            "edges_per_s": sh.m / (ms / 1e3), "count_cold_ms": max_over_ranks(cold[0]), "refinement_trail": trail,
            "rebalance_ms": rebal_ms, "build_ms": bms, "max_rank_resident_bytes": res,
-           "rank_partial": met.triangles, "round_words": round_words}
+           "rank_partial": met.triangles, "round_words": round_words, "run_csv": fh.getvalue().strip().split("\n")}
     del sh
     torch.cuda.empty_cache()
     return out

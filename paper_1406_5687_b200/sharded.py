@@ -860,6 +860,44 @@ def count_gen(sh: ShardGraph, P, rank, ops=None, round_words=1 << 28, met=None, 
     return int(tot[0]), met
 
 
+_MET_FIELDS = ("triangles", "data_msgs_sent", "bytes_sent", "requests_sent", "completion_msgs_sent",
+               "tasks_executed", "partition_bytes", "wire_bytes")
+
+
+def gather_metrics_gen(met: RankMetrics, P, rank, dev=None, busy_ms=0.0):
+    """Every rank's RankMetrics on every rank (the per-rank rows of the
+    reference's run CSV, metrics.py:49-116, from a real N-rank run): one
+    all-reduce of an int64 matrix in which rank r fills row r (counters,
+    busy time in microseconds, data_msgs_to)."""
+    k = len(_MET_FIELDS) + 1
+    row = np.zeros((P, k + P), np.int64)
+    row[rank, : k - 1] = [int(getattr(met, f)) for f in _MET_FIELDS]
+    row[rank, k - 1] = int(round(1e3 * float(busy_ms)))
+    row[rank, k:] = np.asarray(met.data_msgs_to, np.int64)
+    t = torch.as_tensor(row.reshape(-1))
+    t = t.to(dev) if dev is not None else t
+    t = yield ("allreduce", t, "sum")
+    a = (t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)).reshape(P, k + P)
+    out = []
+    for r in range(P):
+        m = RankMetrics(rank=r, nranks=P)
+        for i, f in enumerate(_MET_FIELDS):
+            setattr(m, f, int(a[r, i]))
+        m.busy_time = a[r, k - 1] / 1e6  # seconds
+        m.data_msgs_to = a[r, k:].copy()
+        out.append(m)
+    return out
+
+
+def run_record(total, mets, wall_s, graph="", seed=0, cost="predsum", suite="count"):
+    """The reference's RunRecord (metrics.py:49-83) of one sharded count:
+    algo "surrogate", backend "b200" (time cells are device seconds)."""
+    from .metrics import RunRecord
+
+    return RunRecord(algo="surrogate", ranks=len(mets), cost=cost, graph=graph, seed=seed, backend="b200",
+                     wall_time=wall_s, total=total, rows=list(mets), suite=suite)
+
+
 def slice_of(raw, P, rank):
     """Rank r's slice of a raw pair list and its first pair's index."""
     m = int(raw.shape[0])
@@ -883,6 +921,14 @@ def count_sharded(sh: ShardGraph, group=None, ops=None, round_words=1 << 28):
 
     P, rank = dist.get_world_size(group), dist.get_rank(group)
     return run_dist(count_gen(sh, P, rank, ops, round_words), group)
+
+
+def gather_metrics(met: RankMetrics, group=None, busy_ms=0.0, device=None):
+    """All ranks' RankMetrics on this rank (torch.distributed initialised)."""
+    import torch.distributed as dist
+
+    P, rank = dist.get_world_size(group), dist.get_rank(group)
+    return run_dist(gather_metrics_gen(met, P, rank, device, busy_ms), group)
 
 
 def rebalance_sharded(sh: ShardGraph, busy_ms, group=None, ops=None):

@@ -85,6 +85,9 @@ def test_bench_multi_gpu_path_world1(mode, tmp_path):
         part = line["partitioned"][0]
         assert part.get("error") is None, part
         assert part["triangles"] == 722 and part["triangles_ok"] and part["n_gpus"] == 1
+        # the run CSV of the reference's schema: header + one row per rank
+        assert part["run_csv"][0].startswith("suite,algo,mode,ranks") and len(part["run_csv"]) == 2
+        assert part["run_csv"][1].split(",")[12] == "722" and len(part["refinement_trail"]) == 3
 
 
 def test_capi_nccl_layer_world1():

@@ -96,6 +96,37 @@ def test_sharded_rebalance_emulated_numpy(name):
         assert S.emulate_count(shards, ops=ops)[0] == int(case["T"][0])
 
 
+def test_sharded_run_record_matches_reference_rows():
+    """Per-rank rows of the run CSV from an emulated 3-rank sharded count:
+    gathered by one all-reduce, equal to each rank's own metrics and to the
+    reference's count_space_surrogate rows (triangles, messages, bytes)."""
+    import io
+
+    from paper_1406_5687_b200.metrics import RUN_COLUMNS, write_run_csv
+
+    case = SMALL["pa_500_8_11"]
+    raw = torch.as_tensor(case["raw"].astype(np.int32))
+    ops = NumpyShardOps()
+    P = 3
+    shards, _ = S.emulate_build(raw, P, ops=ops)
+    tot, mets, _ = S.emulate_count(shards, ops=ops)
+    res, _ = S.emulate([S.gather_metrics_gen(mets[r], P, r, busy_ms=1.5 * (r + 1)) for r in range(P)])
+    for r in range(P):  # every rank holds every rank's row
+        assert [m.triangles for m in res[r]] == case["surr_tri_3"].tolist()
+        assert [m.bytes_sent for m in res[r]] == case["surr_bytes_3"].tolist()
+        assert [m.data_msgs_sent for m in res[r]] == case["surr_msgs_3"].tolist()
+        assert np.stack([m.data_msgs_to for m in res[r]]).tolist() == case["surr_census_3"].tolist()
+        assert [m.partition_bytes for m in res[r]] == [m.partition_bytes for m in mets]
+    rec = S.run_record(tot, res[0], 0.004, graph="pa_500_8_11", seed=11)
+    fh = io.StringIO()
+    write_run_csv([rec], fh)
+    rows = [ln.split(",") for ln in fh.getvalue().strip().split("\n")]
+    assert rows[0] == RUN_COLUMNS and len(rows) == 1 + P
+    tri = RUN_COLUMNS.index("triangles")
+    assert [int(r[tri]) for r in rows[1:]] == case["surr_tri_3"].tolist()
+    assert rows[1][RUN_COLUMNS.index("busy_time")] == "0.001500"
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
