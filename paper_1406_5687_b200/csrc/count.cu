@@ -14,25 +14,32 @@
 //
 // Three tiers by table size d (the shape bucketing of SURVEY.md §7 step 6);
 // each tier runs over a compacted list of its own owners:
-//   small  (d <= 128): a warp owns a 2 KB shared slice -- 8K-bit hashed
-//          filter (two bits per id) + bucketized hash table (2^6 buckets of
-//          4 ids) -- and a 4-stage ring its window loads land in by
-//          cp.async, so three windows per warp are in flight without
-//          holding registers;
+//   small  (d <= 128, k_small): a warp owns a 4 KB one-bit hashed filter
+//          and holds the owner's list in registers (4 ids per lane): the
+//          rare filter hits are verified with one shuffle + one ballot, no
+//          bucket table is built; three windows per step are loaded
+//          straight into registers;
 //   mid    (d <= 512): 8 KB slices (32K-bit two-bit filter + 2^8 buckets),
 //          4 warps per block, windows software-pipelined in registers;
 //   block  (d  > 512): a 512-thread block stages up to 4096 ids (256K-bit
 //          filter + 2^11 buckets) and all 16 warps stream the owner's
 //          segments -- the hubs of Chung-Lu / R-MAT; beyond 4096 ids the
 //          probes use binary search in global memory (L1/L2 resident).
-// Segment streaming (all tiers): a warp takes 32 segments, compacts the
-// non-empty ones, and flattens the 16-byte chunks they touch with a warp
-// scan; lane j of a window loads chunk base+j as one int4 (4 list ids),
-// resolving its segment from a shared bitmap of segment starts (popc) or,
-// for groups wider than the bitmap, one ballot + one redux.or + popc.  A
-// probe is one filter LDS and a few ALU ops, branch-free over the 4 ids;
-// only filter hits are verified (one LDS.128 in the bucket table: inline in
-// the warp tiers, queued and verified in bulk in the block tier).
+// Tables whose ids span less than the slice's bit count become exact
+// direct-mapped bitmaps (no hashing, no verification): every block-tier
+// owner of the benchmark graphs.
+// Segment streaming: a warp takes up to 32 segments, compacts the non-empty
+// ones, and flattens the 16-byte chunks they touch with a warp scan; lane j
+// of a window loads chunk base+j as one int4 (4 list ids), resolving its
+// segment from a shared bitmap of segment starts (popc) or, for groups
+// wider than the bitmap, one ballot + one redux.or + popc; the block tier
+// on padded pools carries each lane's segment from window to window instead
+// (stream_group_inc).  A probe is one filter LDS and a few ALU ops,
+// branch-free over the 4 ids; only filter hits are verified (inline in the
+// warp tiers, queued and verified in bulk in the block tier).  On the
+// row-padded pool (tc_build_graph, the sharded ranks' pools) no tier masks
+// ids: whatever a chunk holds outside its segment is <= u or INT32_MAX and
+// cannot be in N^_u.
 //
 // Load balance (the paper's dynamic load balancing, PAPER.md:788-822,
 // dynamic_lb.py:68-109, restated for warps): each tier splits its owners'

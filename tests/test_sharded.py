@@ -148,6 +148,17 @@ def _worker(rank, world, port, name, cost, q):
         sl, base = SS.slice_of(raw, world, rank)
         sh = SS.build_sharded(sl.contiguous(), base, cost=cost, ops=Ops(), keep_maps=True)
         tot, met = SS.count_sharded(sh, ops=Ops(), round_words=16)
+        if cost == "engine":
+            # the measured refinement and the metrics gather over real collectives:
+            # rank 0 "was slow", so its range shrinks; the count must not move
+            b1 = int(sh.bounds[1])
+            sh = SS.rebalance_sharded(sh, 9.0 if rank == 0 else 1.0, ops=Ops())
+            assert int(sh.bounds[1]) < b1
+            tot2, met = SS.count_sharded(sh, ops=Ops(), round_words=64)
+            assert tot2 == tot
+            rows = SS.gather_metrics(met, busy_ms=float(rank + 1))
+            assert [m.rank for m in rows] == list(range(world)) and sum(m.triangles for m in rows) == tot
+            assert rows[rank].bytes_sent == met.bytes_sent and abs(rows[rank].busy_time - (rank + 1) / 1e3) < 1e-9
         q.put((rank, sh.lo, sh.hi, sh.bounds.tolist(), sh.indptr.numpy().tolist(), sh.indices.numpy().tolist(),
                tot, met.triangles, met.data_msgs_to.tolist(), met.bytes_sent, met.data_msgs_sent))
     finally:

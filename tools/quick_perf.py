@@ -18,8 +18,13 @@ ap.add_argument("--configs", default="cfg2")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--lowest", action="store_true")
 ap.add_argument("--no-tiled", action="store_true")
+ap.add_argument("--caps", default="", help="small,mid,block tier caps (tc_set_tuning), e.g. 128,256,4096")
 a = ap.parse_args()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+if a.caps:
+    c = [int(x) for x in a.caps.split(",")]
+    for key, val in ((0, c[0]), (2, c[1]), (1, c[2])):
+        _lib.call("tc_set_tuning", key, val)
 for cfg in a.configs.split(","):
     t0 = time.perf_counter()
     raw = bench.host_raw_edges(cfg, pin=True)
