@@ -150,6 +150,16 @@ int tc_count_middle(const int64_t* tab_indptr, const int32_t* tab_indices,
                     int64_t u0, int64_t u1, const int64_t* bucket_bounds, int32_t nbuckets,
                     unsigned long long* out, tc_stream_t stream);
 
+/* The same total by the formulation BASELINE.json's north_star names: one
+ * warp per oriented edge (v, u), |N^_v ∩ N^_u| by warp merge-path over both
+ * lists staged in shared memory (comparable lengths) or a binary-search
+ * probe of the long list (skewed pairs) -- merge_count summed over the
+ * edges, _kernels.py:15-52, with the merge model's W list steps.  The
+ * measured comparator of the middle-vertex engine, not the
+ * headline path.  out: one uint64. */
+int tc_count_merge_path(const int64_t* eff_indptr, const int32_t* eff_indices, int64_t n, unsigned long long* out,
+                        tc_stream_t stream);
+
 /* Reusable form of tc_count_middle for repeated counts of one graph: the
  * plan (tier lists and chunk boundaries for owners [u0, u1)) is computed
  * once (synchronises); tc_plan_run then only zeroes `out` and launches the

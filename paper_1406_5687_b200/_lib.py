@@ -32,6 +32,7 @@ _SIGS = {
     "tc_normalize_host": [_vp, _i64, _vp, _vp, _pi64, _pi64, _vp, _vp, _vp],
     "tc_build_full": [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "tc_count_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
+    "tc_count_merge_path": [_vp, _vp, _i64, _vp, _vp],
     "tc_count_lowest": [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp],
     "tc_plan_middle": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp, _i32, ctypes.POINTER(_vp), _vp],
     "tc_plan_run": [_vp, _vp, _vp],

@@ -129,6 +129,18 @@ def count_lowest(g: Graph, v0=0, v1=None, bounds=None, out=None):
     return out
 
 
+def count_merge_path(g: Graph, out=None):
+    """count_node_range(0, n) by warp-per-edge merge-path / binary-search
+    intersections (merge_count per oriented edge, _kernels.py:15-52): the
+    formulation the north star names, kept as the measured comparator of
+    the middle-vertex engine."""
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64, device=g.eff_indptr.device)
+    _lib.call("tc_count_merge_path", _lib.ptr(g.eff_indptr), _lib.ptr(g.eff_indices), g.n, _lib.ptr(out),
+              _lib.stream())
+    return out
+
+
 def count_triangles_seq(g: Graph) -> int:
     """Exact triangle count of g (sequential.py:30-34)."""
     if g.n < 3:

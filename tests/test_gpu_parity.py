@@ -11,7 +11,7 @@ from conftest import SMALL, SMALL_NAMES
 import paper_1406_5687_b200 as tcb
 from paper_1406_5687_b200 import graph as G
 from paper_1406_5687_b200.graph_io import er_edges, pa_edges_host, rmat_edges
-from paper_1406_5687_b200.sequential import count_lowest, count_middle, count_middle_part
+from paper_1406_5687_b200.sequential import count_lowest, count_merge_path, count_middle, count_middle_part
 from oracle import gen_twin
 from oracle import oracle as O
 
@@ -342,6 +342,31 @@ def test_engine_tiers_forced(caps):
         L.tc_set_tuning(0, -1)
         L.tc_set_tuning(2, -1)
         L.tc_set_tuning(1, -1)
+
+
+@pytest.mark.parametrize("name", SMALL_NAMES)
+def test_merge_path_engine(name):
+    """The north star's literal formulation (warp per oriented edge, merge-path
+    or binary-search intersection) gives the reference's total on every
+    fixture."""
+    _, g = graph_of(name)
+    assert int(count_merge_path(g).item()) == int(SMALL[name]["T"][0])
+
+
+def test_merge_path_engine_shapes():
+    """Long lists (not staged), skewed pairs (binary-search probe) and a dense
+    core (merge-path over hundreds of ids) against the oracle."""
+    rng = np.random.default_rng(11)
+    core = np.array([(a, b) for a in range(1100) for b in range(a + 1, 1100) if (a * 31 + b * 17) % 3], np.int64)
+    stars = np.stack([rng.integers(0, 40, 30000), rng.integers(1100, 9000, 30000)], 1)
+    extra = rng.integers(0, 9000, size=(60000, 2))
+    raw = np.concatenate([core, stars, extra])
+    og = O.build_graph(*O.normalize(raw))
+    assert int(og.eff_deg.max()) > 512
+    g = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(raw)))
+    T = O.count_triangles(og)
+    assert int(count_merge_path(g).item()) == T
+    assert tcb.count_triangles_seq(g) == T
 
 
 def test_block_tier_hashed_tables_wide_spans():

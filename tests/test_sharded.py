@@ -209,7 +209,7 @@ def test_sharded_device_emulated(name):
             continue
         shards, _ = S.emulate_build(raw, P, keep_maps=True)
         _check_build(case, shards, P)
-        for rw in (64, 1 << 27):
+        for rw in (64, 1 << 27, 64):  # the third count re-uses the kept round plans (index_emit + rebind)
             tot, mets, _ = S.emulate_count(shards, round_words=rw)
             _check_count(case, tot, mets, P)
         eshards, _ = S.emulate_build(raw, P, cost="engine")
@@ -232,7 +232,16 @@ def test_sharded_device_cfg2(configs, P):
     del raw
     assert shards[0].bounds.tolist() == c[f"bounds_predsum_{P}"]
     assert sum(sh.m_local for sh in shards) == c["m"]
-    tot, mets, _ = S.emulate_count(shards, round_words=1 << 22)
-    assert tot == c["T"]
-    assert [m.triangles for m in mets] == c[f"surr_tri_{P}"]
-    assert np.stack([m.data_msgs_to for m in mets]).tolist() == c[f"surr_census_{P}"]
+    for rep in range(2):  # the second count runs on the kept send plan, exchange plan and round plans
+        tot, mets, _ = S.emulate_count(shards, round_words=1 << 22)
+        assert tot == c["T"]
+        assert [m.triangles for m in mets] == c[f"surr_tri_{P}"]
+        assert np.stack([m.data_msgs_to for m in mets]).tolist() == c[f"surr_census_{P}"]
+    # the pack is deterministic: two packs of one shard are byte-identical
+    ops = S.ShardOps()
+    sh = shards[0]
+    sd, sz = ops.send_sizes(sh, P, 0)
+    a = ops.send_pack(sh, P, 0, sd, int(sz[0].sum()), int(sz[1].sum()))
+    b = ops.send_pack(sh, P, 0, sd, int(sz[0].sum()), int(sz[1].sum()))
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    assert int(a[0].sum()) <= int(sz[1].sum()) and int((a[0] > 0).all())

@@ -18,6 +18,7 @@ ap.add_argument("--configs", default="cfg2")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--lowest", action="store_true")
 ap.add_argument("--no-tiled", action="store_true")
+ap.add_argument("--merge", action="store_true", help="also time the warp-per-edge merge-path comparator")
 ap.add_argument("--caps", default="", help="small,mid,block tier caps (tc_set_tuning), e.g. 128,256,4096")
 a = ap.parse_args()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -41,6 +42,18 @@ for cfg in a.configs.split(","):
     engines = [("middle", lambda: count_middle(g, tiled=False))]
     engines += [] if a.no_tiled else [("tiled", lambda: count_middle(g, tiled=True))]
     engines += [("lowest", lambda: count_lowest(g))] if a.lowest else []
+    if a.merge:
+        from paper_1406_5687_b200.sequential import count_merge_path
+        T0 = int(count_middle(g, tiled=False).item())
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        assert int(count_merge_path(g).item()) == T0
+        flush.fill_(1)
+        ev[0].record()
+        count_merge_path(g)
+        ev[1].record()
+        torch.cuda.synchronize()
+        print(f"{cfg} merge-path: T={T0} {ev[0].elapsed_time(ev[1]):.3f} ms -> {g.m / ev[0].elapsed_time(ev[1]) / 1e6:.2f} G edges/s",
+              flush=True)
     from paper_1406_5687_b200.graph import tiled_index
     import paper_1406_5687_b200.graph as G
     if G.TILE_IDS == 0:
