@@ -685,6 +685,9 @@ __device__ __forceinline__ void stream_group_inc(const Segs& segs, const int32_t
           sEnd = q.z;
           sPtr = reinterpret_cast<const int4*>(((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x);
         }
+#if TCB_DEBUG
+        assert(sj < nseg && f < sEnd && (sj == 0 || f >= segtab[sj - 1].z));
+#endif
         p = sPtr + f;
       }
       v[k] = __ldg(p);

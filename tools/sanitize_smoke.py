@@ -49,5 +49,10 @@ T = tcb.count_triangles_seq(gh)
 for cost in ("predsum", "engine"):
     shards, _ = S.emulate_build(raw, 3, cost=cost)
     assert S.emulate_count(shards, round_words=256)[0] == T
+    assert S.emulate_count(shards, round_words=256)[0] == T  # kept round plans: index_emit + rebind
+    shards = S.emulate_rebalance(shards, [3.0, 1.0, 2.0])
+    assert S.emulate_count(shards)[0] == T
+from paper_1406_5687_b200.sequential import count_merge_path  # noqa: E402
+assert int(count_merge_path(gh).item()) == T
 torch.cuda.synchronize()
 print("sanitize workload ok")
