@@ -281,6 +281,17 @@ def count_space_surrogate_dist(g, cost=None, group=None, ops=None):
     P = dist.get_world_size(group)
     rank = dist.get_rank(group)
     bounds = range_bounds(partition_ranges(g, cost, P))
+    if ops is None:
+        # the sharded pipeline's count (sharded.py): sizes, lengths and
+        # plans stay on the device / on the shard, bounded exchange rounds,
+        # the local engine overlapping the exchange; same partials and census
+        from . import sharded as S
+
+        key = ("surrogate_shard", P, rank, str(cost))
+        sh = g._cache.get(key)
+        if sh is None:
+            sh = g._cache[key] = S.shard_from_graph(g, bounds, rank)
+        return S.count_sharded(sh, group=group)
     shard = shard_of(g, int(bounds[rank]), int(bounds[rank + 1]))
     return surrogate_rank(shard, bounds, group=group, ops=ops)
 

@@ -898,6 +898,22 @@ def run_record(total, mets, wall_s, graph="", seed=0, cost="predsum", suite="cou
                      wall_time=wall_s, total=total, rows=list(mets), suite=suite)
 
 
+def shard_from_graph(g, bounds, rank, ops=None) -> ShardGraph:
+    """Rank `rank`'s ShardGraph cut out of a whole (replicated) Graph: its
+    forward lists and the engine's padded copy of them.  For callers of the
+    reference-style API that already hold the graph on every rank
+    (distributed.count_space_surrogate_dist)."""
+    ops = ops or ShardOps()
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    e0, e1 = int(g.eff_indptr[lo]), int(g.eff_indptr[hi])
+    indptr = (g.eff_indptr[lo: hi + 1] - e0).contiguous()
+    buf = torch.zeros(e1 - e0 + 4, dtype=torch.int32, device=indptr.device)  # +4: 16-byte chunk reads
+    buf[: e1 - e0] = g.eff_indices[e0:e1]
+    indices = buf[: e1 - e0]
+    pip, pool = ops.pool(indptr, indices)
+    return ShardGraph(lo, hi, int(g.n), int(g.m), np.asarray(bounds, np.int64), indptr, indices, pip, pool)
+
+
 def slice_of(raw, P, rank):
     """Rank r's slice of a raw pair list and its first pair's index."""
     m = int(raw.shape[0])

@@ -156,3 +156,20 @@ def test_partitioned_schemes_tiny_graphs_oracle(known):
             dp, dreq, dwords = O.direct(g, b)
             assert dp.tolist() == dire["triangles"] and dreq.tolist() == dire["requests_to"], (name, P)
             assert (8 * (2 * dreq.sum(1) + dwords + (P - 1))).tolist() == dire["bytes_sent"], (name, P)
+
+
+def test_scale_goldens_reference_pin():
+    """Where the reference itself was run at a full-size config
+    (tests/golden/make_reference_scale.py adds a "reference" block to
+    scale.json), its graph and count equal the oracle's numbers the GPU tests
+    compare against."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "scale.json")
+    scale = json.load(open(path))
+    pinned = [c for c in scale if "reference" in scale[c]]
+    for c in pinned:
+        ref = scale[c]["reference"]
+        for k in ("n", "m", "T", "relabel_checksum", "eff_indptr_checksum", "eff_indices_checksum"):
+            assert ref[k] == scale[c][k], (c, k)

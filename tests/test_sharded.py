@@ -214,6 +214,12 @@ def test_sharded_device_emulated(name):
             _check_count(case, tot, mets, P)
         eshards, _ = S.emulate_build(raw, P, cost="engine")
         assert S.emulate_count(eshards)[0] == int(case["T"][0])
+        if P == 3:  # shards cut out of a replicated Graph (count_space_surrogate_dist's path)
+            import paper_1406_5687_b200 as tcb
+            g = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(case["raw"])))
+            gsh = [S.shard_from_graph(g, case["bounds_predsum_3"], r) for r in range(P)]
+            tot, mets, _ = S.emulate_count(gsh)
+            _check_count(case, tot, mets, P)
         eshards = S.emulate_rebalance(eshards, [float(1 + (r % 3)) for r in range(P)])
         _check_rebalanced(case, eshards, P)
         assert S.emulate_count(eshards, round_words=64)[0] == int(case["T"][0])

@@ -1,7 +1,7 @@
 #!/bin/bash
-# tools/r20_measure.sh TAG -- the full measurement set of HEAD on a B200 (via gpurun): gpu tests, smoke, both bench
+# tools/final_measure.sh TAG -- the full measurement set of HEAD on a B200 (via gpurun): gpu tests, smoke, both bench
 # arms, launch list, engine ncu captures (sha-stamped DRAM bytes), e2e kernels, sharded-pipeline emulation.
-TAG=${1:-r20}
+TAG=${1:-r22}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt 2>&1
