@@ -71,11 +71,15 @@ def test_bench_multi_gpu_path_world1(mode, tmp_path):
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, TCB_BENCH_DIST="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(repo, "bench.py"),
-           "--gpus", "1", "--steps", "2", "--warmup", "3", "--mode", mode, "--no-e2e", "--no-cpu-baseline",
-           "--config", "cfg1", "--partitioned", "cfg1" if mode == "replicated" else ""]
-    out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+    for attempt in range(3):  # a rendezvous port can be taken between _port() and torchrun's bind
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(repo, "bench.py"),
+               "--gpus", "1", "--steps", "2", "--warmup", "3", "--mode", mode, "--no-e2e", "--no-cpu-baseline",
+               "--config", "cfg1", "--partitioned", "cfg1" if mode == "replicated" else ""]
+        out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=600)
+        transient = ("address already in use", "eaddrinuse", "connection refused", "rendezvous", "timed out")
+        if out.returncode == 0 or not any(t in out.stderr.lower() for t in transient):
+            break
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["workload_detail"]["triangles"] == 722 and line["n_gpus"] == 1
