@@ -257,12 +257,23 @@ __global__ void k_eff_counts(const int32_t* __restrict__ deg_orig, const int32_t
 // scatter runs in phases over row ranges [bounds[ph], bounds[ph+1]) whose
 // slots span about the same number of entries, so each phase's writes land
 // in an L2-resident window of the output instead of random DRAM sectors.
-__global__ void k_orient_scatter(const int2* __restrict__ lohi, int64_t m, const int64_t* __restrict__ indptr,
-                                 const int64_t* __restrict__ bounds, int ph, int32_t* cursor, int32_t* out) {
+// cursor[v] starts at row v's first slot (k_cursor_init; m < 2^31), so a
+// slot costs one atomic and no read of indptr.
+__global__ void k_orient_scatter(const int2* __restrict__ lohi, int64_t m, const int64_t* __restrict__ bounds,
+                                 int ph, int32_t* cursor, int32_t* out) {
   const int64_t r0 = bounds[ph], r1 = bounds[ph + 1];
   GRID_STRIDE(i, m) {
     const int2 k = lohi[i];
-    if (k.x >= r0 && k.x < r1) out[indptr[k.x] + atomicAdd(&cursor[k.x], 1)] = k.y;
+    if (k.x >= r0 && k.x < r1) out[atomicAdd(&cursor[k.x], 1)] = k.y;
+  }
+}
+
+// front[v] = indptr[v]; back[v] (nullable) = indptr[v + 1] - 1: the slot
+// cursors of the counting scatters as absolute positions.
+__global__ void k_cursor_init(const int64_t* __restrict__ indptr, int64_t n, int32_t* front, int32_t* back) {
+  GRID_STRIDE(v, n) {
+    front[v] = (int32_t)indptr[v];
+    if (back) back[v] = (int32_t)(indptr[v + 1] - 1);
   }
 }
 
@@ -343,8 +354,8 @@ __global__ void k_rev_scatter(const int64_t* __restrict__ eff_indptr, const int3
           for (int64_t q = p0 + (wend - wbeg); q < pool_indptr[w + 1]; ++q) pool[q] = INT32_MAX;
       }
       if (u < u0 || u >= u1) continue;
-      const int64_t slot = (e + 1 < wend) ? rev_indptr[u] + atomicAdd(&cursor[u], 1)
-                                          : rev_indptr[u + 1] - 1 - atomicAdd(&back[u], 1);
+      // front / back cursors hold absolute slots (k_cursor_init)
+      const int64_t slot = (e + 1 < wend) ? atomicAdd(&cursor[u], 1) : atomicSub(&back[u], 1);
 #if TCB_DEBUG
       assert(slot >= rev_indptr[u] && slot < rev_indptr[u + 1]);
 #endif
@@ -1061,17 +1072,17 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, cin, cout, n + 1, s));
     if (m) {
       int32_t* unsorted = sc.alloc<int32_t>(m);
+      TC_REQUIRE(m < (1ll << 31), TC_EINVAL, "m must be < 2^31");
       int32_t* cursor = sc.alloc<int32_t>(n);
-      TC_CUDA(cudaMemsetAsync(cursor, 0, n * sizeof(int32_t), s));
+      k_cursor_init<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, n, cursor, nullptr);
+      check_launch();
       const int nph = scatter_phases(m * 4);
       k_phase_bounds<<<1, 32, 0, s>>>(eff_indptr, n, nph, bounds);
       check_launch();
       for (int ph = 0; ph < nph; ++ph) {
-        k_orient_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(lohi, m, eff_indptr, bounds, ph, cursor,
-                                                                          unsorted);
+        k_orient_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(lohi, m, bounds, ph, cursor, unsorted);
         check_launch();
       }
-      TC_REQUIRE(m < (1ll << 31), TC_EINVAL, "m must be < 2^31");
       int64_t* seg_end = sc.alloc<int64_t>(n);
       int32_t* rows = sc.alloc<int32_t>(5 * n);
       int* counts = sc.alloc<int>(5);
@@ -1121,7 +1132,8 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
   }
   if (m) {
     int32_t* cursor = sc.alloc<int32_t>(2 * n);
-    TC_CUDA(cudaMemsetAsync(cursor, 0, 2 * n * sizeof(int32_t), s));
+    k_cursor_init<<<grid_for(n, kBlock), kBlock, 0, s>>>(rev_indptr, n, cursor, cursor + n);
+    check_launch();
     const int nph = scatter_phases(m * 8, (int64_t)TCB_REV_WINDOW_MB << 20);
     k_phase_bounds<<<1, 32, 0, s>>>(rev_indptr, n, nph, bounds);
     check_launch();
