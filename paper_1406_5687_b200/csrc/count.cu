@@ -60,6 +60,23 @@ namespace tcb {
 #ifndef TCB_BIG_INC_PIPE
 #define TCB_BIG_INC_PIPE 0
 #endif
+// chunk schedule of the warp tiers (k_plan, mode 1): uniform chunks per worker
+// over the first TCB_PLAN_HALF of the cost, smallest chunk = cost / (MINDIV * workers)
+#ifndef TCB_PLAN_FIRST
+#define TCB_PLAN_FIRST 6
+#endif
+#ifndef TCB_PLAN_HALF
+#define TCB_PLAN_HALF 0.75
+#endif
+#ifndef TCB_PLAN_MINDIV
+#define TCB_PLAN_MINDIV 256.0  // 32 -> 256: finer tail chunks, cfg 2 1.68 -> 1.61 ms, cfg 5 small tier 11.95 -> 11.47
+#endif
+#ifndef TCB_PLAN_SEG_MINDIV
+#define TCB_PLAN_SEG_MINDIV 32.0  // the block tier's plan (k_plan_seg)
+#endif
+#ifndef TCB_PLAN_NMAX
+#define TCB_PLAN_NMAX 16  // chunk slots per worker (first + geometric + tail chunks must fit)
+#endif
 #ifndef TCB_MINBLOCKS
 #define TCB_MINBLOCKS 5
 #endif
@@ -1457,11 +1474,11 @@ __global__ void k_plan(const int64_t* __restrict__ cp, const int64_t* __restrict
   const int64_t base = cp[x0];
   const int64_t C = cp[x1] - base;
   const double Cd = (double)C;
-  const int nfirst = mode == 0 ? nW : 6 * nW;
-  const double half = mode == 0 ? floor(Cd / 2.0) : floor(Cd * 0.75);
+  const int nfirst = mode == 0 ? nW : TCB_PLAN_FIRST * nW;
+  const double half = mode == 0 ? floor(Cd / 2.0) : floor(Cd * TCB_PLAN_HALF);
   const double R0 = Cd - half;
   const double q = 1.0 - 1.0 / (double)nW;
-  const double minc = fmax(Cd / (32.0 * nW), 64.0);
+  const double minc = fmax(Cd / (TCB_PLAN_MINDIV * nW), 64.0);
   int64_t J = 0;
   if (nW > 1 && R0 / nW > minc) J = (int64_t)ceil(log(minc * nW / R0) / log(q));
   if (J < 0) J = 0;
@@ -1640,7 +1657,7 @@ __global__ void k_plan_seg(const int64_t* __restrict__ sp, int64_t nseg, const i
   const double half = floor(Cd * 0.75);
   const double R0 = Cd - half;
   const double q = 1.0 - 1.0 / (double)nW;
-  const double minc = fmax(Cd / (32.0 * nW), 64.0);
+  const double minc = fmax(Cd / (TCB_PLAN_SEG_MINDIV * nW), 64.0);
   int64_t J = 0;
   if (nW > 1 && R0 / nW > minc) J = (int64_t)ceil(log(minc * nW / R0) / log(q));
   if (J < 0) J = 0;
@@ -1798,7 +1815,7 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
     TC_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp2, cst, vcost, nx + 1, s));
     // planned for the workers of all `parts` devices that split the chunks
     const int nW = ts.workers[k] * parts;
-    const int nmax = 10 * nW + 8;
+    const int nmax = TCB_PLAN_NMAX * nW + 8;
     int64_t* chunk_r = al.template alloc<int64_t>(nmax + 1);
     int32_t* chunk_x = al.template alloc<int32_t>(nmax);
     int* ctl = al.template alloc<int>(2);  // [0] nchunks, [1] queue
