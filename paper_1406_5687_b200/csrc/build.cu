@@ -991,6 +991,37 @@ void normalize_host(const int32_t* host, int64_t m_raw, int32_t* dev, int32_t* o
   if (deg_valid) *deg_valid = (*m_host == m_raw && *n_host == L1) ? 1 : 0;
 }
 
+// Sorts every CSR row (ascending ids) from `unsorted` into `out`, by row
+// length class: CUB's segmented sort for the shortest rows, warp / block
+// sorting networks for the rest (k_row_classes empties the segments the
+// class kernels own).  Shared by tc_build_graph and the sharded build
+// (tc_shard_csr).
+void sort_rows(Scratch& sc, const int64_t* indptr, int64_t n, int64_t m, const int32_t* unsorted, int32_t* out,
+               cudaStream_t s) {
+  if (n <= 0 || m <= 0) return;
+  const int sms = sm_count();
+  int64_t* seg_end = sc.alloc<int64_t>(n);
+  int32_t* rows = sc.alloc<int32_t>(5 * n);
+  int* counts = sc.alloc<int>(5);
+  TC_CUDA(cudaMemsetAsync(counts, 0, 5 * sizeof(int), s));
+  k_row_classes<<<grid_for(n, kBlock), kBlock, 0, s>>>(indptr, n, seg_end, rows, n, counts);
+  check_launch();
+  size_t tmp2 = 0;
+  TC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp2, unsorted, out, (int)m, (int)n, indptr, seg_end, s));
+  void* t2 = sc.bytes(tmp2);
+  TC_CUDA(cub::DeviceSegmentedSort::SortKeys(t2, tmp2, unsorted, out, (int)m, (int)n, indptr, seg_end, s));
+  k_sort_rows_warp<8><<<sms * 8, 256, 0, s>>>(indptr, unsorted, out, rows, counts);
+  check_launch();
+  k_sort_rows_warp<16><<<sms * 8, 256, 0, s>>>(indptr, unsorted, out, rows + n, counts + 1);
+  check_launch();
+  k_sort_rows_warp<32><<<sms * 4, 256, 0, s>>>(indptr, unsorted, out, rows + 2 * n, counts + 2);
+  check_launch();
+  k_sort_rows_block<256, 8><<<sms * 4, 256, 0, s>>>(indptr, unsorted, out, rows + 3 * n, counts + 3);
+  check_launch();
+  k_sort_rows_block<512, kBlockRowMax / 512><<<sms * 2, 512, 0, s>>>(indptr, unsorted, out, rows + 4 * n, counts + 4);
+  check_launch();
+}
+
 // ---------------------------------------------------------------- build
 
 void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* order,
@@ -1083,29 +1114,7 @@ void build_graph(const int32_t* edges, int64_t m, int64_t n, const int32_t* orde
         k_orient_scatter<<<grid_for(m, kBlock, sms * 16), kBlock, 0, s>>>(lohi, m, bounds, ph, cursor, unsorted);
         check_launch();
       }
-      int64_t* seg_end = sc.alloc<int64_t>(n);
-      int32_t* rows = sc.alloc<int32_t>(5 * n);
-      int* counts = sc.alloc<int>(5);
-      TC_CUDA(cudaMemsetAsync(counts, 0, 5 * sizeof(int), s));
-      k_row_classes<<<grid_for(n, kBlock), kBlock, 0, s>>>(eff_indptr, n, seg_end, rows, n, counts);
-      check_launch();
-      size_t tmp2 = 0;
-      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp2, unsorted, eff_indices, (int)m, (int)n, eff_indptr,
-                                                 seg_end, s));
-      void* t2 = sc.bytes(tmp2);
-      TC_CUDA(cub::DeviceSegmentedSort::SortKeys(t2, tmp2, unsorted, eff_indices, (int)m, (int)n, eff_indptr,
-                                                 seg_end, s));
-      k_sort_rows_warp<8><<<sms * 8, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows, counts);
-      check_launch();
-      k_sort_rows_warp<16><<<sms * 8, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + n, counts + 1);
-      check_launch();
-      k_sort_rows_warp<32><<<sms * 4, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + 2 * n, counts + 2);
-      check_launch();
-      k_sort_rows_block<256, 8><<<sms * 4, 256, 0, s>>>(eff_indptr, unsorted, eff_indices, rows + 3 * n, counts + 3);
-      check_launch();
-      k_sort_rows_block<512, kBlockRowMax / 512><<<sms * 2, 512, 0, s>>>(eff_indptr, unsorted, eff_indices,
-                                                                         rows + 4 * n, counts + 4);
-      check_launch();
+      sort_rows(sc, eff_indptr, n, m, unsorted, eff_indices, s);
     }
   }
   int64_t* in_deg = sc.alloc<int64_t>(n + 1);

@@ -118,6 +118,10 @@ inline void check_launch() {
   TC_CUDA(cudaGetLastError());
 }
 
+// Every row of a CSR sorted ascending, unsorted -> out (build.cu).
+void sort_rows(Scratch& sc, const int64_t* indptr, int64_t n, int64_t m, const int32_t* unsorted, int32_t* out,
+               cudaStream_t s);
+
 // Row of forward edge e: the largest v with indptr[v] <= e (indptr[n] = m > e).
 __device__ __forceinline__ int64_t row_of_edge(const int64_t* __restrict__ indptr, int64_t n, int64_t e) {
   int64_t lo = 0, hi = n;

@@ -104,8 +104,22 @@ __device__ __forceinline__ int dest_of_key(unsigned long long key, int P) {
   return (int)(((key * 0x9E3779B97F4A7C15ull) >> 33) % (unsigned long long)P);
 }
 
+// Per-destination counters of a block (P <= kMaxDest): elements are counted
+// in shared memory and every block adds its totals once -- one global atomic
+// per element on P addresses serialised the whole grid (35 ms per 64 M pairs).
+static constexpr int kMaxDest = 1024;
+
+__device__ __forceinline__ void flush_counts(const unsigned int* sc, int P, long long* counts) {
+  __syncthreads();
+  for (int j = threadIdx.x; j < P; j += blockDim.x)
+    if (sc[j]) add64(&counts[j], (long long)sc[j]);
+}
+
 __global__ void k_sh_keys(const int2* __restrict__ pairs, int64_t m, const int32_t* __restrict__ map, int P,
                           unsigned long long* key, int32_t* dest, long long* counts) {
+  __shared__ unsigned int sc[kMaxDest];
+  for (int j = threadIdx.x; j < P; j += blockDim.x) sc[j] = 0;
+  __syncthreads();
   GRID_STRIDE(i, m) {
     const int2 e = pairs[i];
     int d = -1;
@@ -114,29 +128,46 @@ __global__ void k_sh_keys(const int2* __restrict__ pairs, int64_t m, const int32
       const uint32_t a = (uint32_t)(map ? map[e.x] : e.x), b = (uint32_t)(map ? map[e.y] : e.y);
       k = ((unsigned long long)min(a, b) << 32) | max(a, b);
       d = dest_of_key(k, P);
-      add64(&counts[d], 1ll);
+      atomicAdd(&sc[d], 1u);
     }
     key[i] = k;
     dest[i] = d;
   }
+  flush_counts(sc, P, counts);
 }
 
-// scatter into groups by destination (order inside a group unspecified)
+// scatter into groups by destination (order inside a group unspecified):
+// per tile of blockDim elements the block counts its destinations in shared
+// memory (the atomic's return value is the element's rank in the tile),
+// reserves one range per destination with one global atomic, and writes.
 template <class T>
 __global__ void k_sh_group(const T* __restrict__ in, const int32_t* __restrict__ dest, int64_t m,
                            const long long* __restrict__ counts, const long long* __restrict__ off, long long* cursor,
-                           T* out) {
-  GRID_STRIDE(i, m) {
-    const int d = dest[i];
-    if (d < 0) continue;
-    const long long c = add64(&cursor[d], 1ll);
+                           T* out, int P) {
+  __shared__ unsigned int sc[kMaxDest];
+  __shared__ long long sbase[kMaxDest];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {  // block-uniform trip count
+    for (int j = threadIdx.x; j < P; j += blockDim.x) sc[j] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    const int d = i < m ? dest[i] : -1;
+    unsigned int r = 0;
+    if (d >= 0) r = atomicAdd(&sc[d], 1u);
+    __syncthreads();
+    for (int j = threadIdx.x; j < P; j += blockDim.x)
+      if (sc[j]) {
+        const long long c = add64(&cursor[j], (long long)sc[j]);
 #if TCB_DEBUG
-    assert(c < counts[d]);
-#else
-    (void)counts;
+        assert(c + sc[j] <= counts[j]);
 #endif
-    out[off[d] + c] = in[i];
+        sbase[j] = off[j] + c;
+      }
+    __syncthreads();
+    if (d >= 0) out[sbase[d] + r] = in[i];
+    __syncthreads();
   }
+  (void)counts;
 }
 
 __global__ void k_sh_unique_flags(const unsigned long long* __restrict__ k, int64_t n, uint8_t* f) {
@@ -189,11 +220,15 @@ __device__ __forceinline__ int owner_of_id(const int64_t* __restrict__ bounds, i
 
 __global__ void k_sh_route_dest(const int2* __restrict__ lohi, int64_t k, const int64_t* __restrict__ bounds, int P,
                                 int32_t* dest, long long* counts) {
+  __shared__ unsigned int sc[kMaxDest];
+  for (int j = threadIdx.x; j < P; j += blockDim.x) sc[j] = 0;
+  __syncthreads();
   GRID_STRIDE(i, k) {
     const int d = owner_of_id(bounds, P, lohi[i].x);
     dest[i] = d;
-    add64(&counts[d], 1ll);
+    atomicAdd(&sc[d], 1u);
   }
+  flush_counts(sc, P, counts);
 }
 
 __global__ void k_sh_row_count(const int2* __restrict__ lohi, int64_t k, int64_t lo, long long* cnt) {
@@ -651,7 +686,7 @@ int tc_shard_keys(const int32_t* pairs, int64_t m, const int32_t* map, int32_t P
     check_launch();
     ex_sum(sc, cnt, cnt + P, P, s);
     k_sh_group<<<grid_for(m, kBlk), kBlk, 0, s>>>(key, dest, m, cnt, cnt + P, cnt + 2 * P,
-                                                 reinterpret_cast<unsigned long long*>(keys_out));
+                                                 reinterpret_cast<unsigned long long*>(keys_out), P);
     check_launch();
     TC_CUDA(cudaMemcpyAsync(counts_host, cnt, P * sizeof(long long), cudaMemcpyDeviceToHost, s));
     sync_stream(s);
@@ -763,7 +798,7 @@ int tc_shard_route(const int32_t* lohi, int64_t k, const int64_t* bounds, int32_
     check_launch();
     ex_sum(sc, cnt, cnt + P, P, s);
     k_sh_group<<<grid_for(k, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(lohi), dest, k, cnt, cnt + P, cnt + 2 * P,
-                                                 reinterpret_cast<int2*>(out));
+                                                 reinterpret_cast<int2*>(out), P);
     check_launch();
     TC_CUDA(cudaMemcpyAsync(counts_host, cnt, P * sizeof(long long), cudaMemcpyDeviceToHost, s));
     sync_stream(s);
@@ -790,11 +825,7 @@ int tc_shard_csr(const int32_t* lohi, int64_t k, int64_t lo, int64_t nrow, int64
     k_sh_row_scatter<<<grid_for(k, kBlk), kBlk, 0, s>>>(reinterpret_cast<const int2*>(lohi), k, lo, indptr, cur,
                                                        unsorted);
     check_launch();
-    size_t tmp = 0;
-    TC_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, unsorted, indices, (int)k, (int)nrow, indptr, indptr + 1,
-                                               s));
-    void* t = sc.bytes(tmp);
-    TC_CUDA(cub::DeviceSegmentedSort::SortKeys(t, tmp, unsorted, indices, (int)k, (int)nrow, indptr, indptr + 1, s));
+    sort_rows(sc, indptr, nrow, k, unsorted, indices, s);  // the length-classed row sorts of tc_build_graph
   });
 }
 

@@ -697,12 +697,14 @@ def _repartition(indptr, indices, lo, hi, nb, P, dev):
     lens = (indptr[1:] - indptr[:-1]).to(torch.int32)
     rc = np.zeros(P, np.int64)
     ic = np.zeros(P, np.int64)
-    ip = indptr.cpu().numpy() if isinstance(indptr, torch.Tensor) else indptr
+    # row offsets at the new bounds only (2 P entries, not the whole offsets array)
+    cuts = np.array([[min(max(int(nb[j]), lo), hi) - lo, min(max(int(nb[j + 1]), lo), hi) - lo] for j in range(P)],
+                    np.int64)
+    at = indptr[torch.as_tensor(cuts.reshape(-1)).to(indptr.device)].cpu().numpy().reshape(P, 2)
     for j in range(P):
-        a, b = max(lo, int(nb[j])), min(hi, int(nb[j + 1]))
-        if a < b:
-            rc[j] = b - a
-            ic[j] = int(ip[b - lo] - ip[a - lo])
+        if cuts[j, 0] < cuts[j, 1]:
+            rc[j] = cuts[j, 1] - cuts[j, 0]
+            ic[j] = int(at[j, 1] - at[j, 0])
     rl, _ = yield ("a2a", lens.contiguous(), rc)
     ri, _ = yield ("a2a", indices.contiguous(), ic)
     nip = torch.zeros(int(rl.numel()) + 1, dtype=torch.int64, device=dev)
