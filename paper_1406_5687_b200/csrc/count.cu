@@ -112,7 +112,10 @@ static constexpr int kBigStages = TCB_BIG_STAGES;  // block tier, exact tables: 
 #ifndef TCB_WINDOWS
 #define TCB_WINDOWS 2
 #endif
-static constexpr int kWarps = 8;          // warps per block (small tier)
+#ifndef TCB_SMALL_WARPS
+#define TCB_SMALL_WARPS 7  // x 6 blocks = 42 warps per SM at 40 registers (8 x 5 = 40 warps at 48: cfg 2 1.63 -> 1.60 ms)
+#endif
+static constexpr int kWarps = TCB_SMALL_WARPS;  // warps per block (small tier)
 static constexpr int kWin = TCB_WINDOWS;  // 32-chunk windows in flight per warp
 static constexpr int kThreads = kWarps * 32;
 #ifndef TCB_SMALL_CAP
@@ -1011,7 +1014,7 @@ __global__ void __launch_bounds__(kWPB * 32, kMinB) k_engine(EngineArgs a, Segs 
 #define TCB_SMALL_PIPE2 0  // issue the next step's loads before probing the current one
 #endif
 #ifndef TCB_SMALL_MINB
-#define TCB_SMALL_MINB 5
+#define TCB_SMALL_MINB 6
 #endif
 #ifndef TCB_SMALL_LWS
 #define TCB_SMALL_LWS 10  // filter words = 2^10 (32K bits, 4 KB per warp); exact spans < 32 * 2^10 ids
