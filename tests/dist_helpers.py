@@ -111,7 +111,7 @@ class NumpyShardOps:
 
     @staticmethod
     def _np(t):
-        return t.numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+        return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
 
     def minmax(self, pairs):
         p = self._np(pairs)
