@@ -152,6 +152,13 @@ static constexpr int kPosCap = TCB_POS_CAP;  // block tier: per-warp queue of fi
 #define TCB_BIG_WINDOWS 3  // block tier: windows in flight per warp (2 -> 3: cfg 4 block tier 114.0 -> 106.4 ms)
 #endif
 static constexpr int kBigWin = TCB_BIG_WINDOWS;
+#ifndef TCB_BIG_WINDOWS_EXACT
+#define TCB_BIG_WINDOWS_EXACT 4  // the exact-only form (no hit queue)
+#endif
+#ifndef TCB_BIG_EXACT_PIPE
+#define TCB_BIG_EXACT_PIPE true
+#endif
+static constexpr int kBigWinExact = TCB_BIG_WINDOWS_EXACT;
 static constexpr int kPosDrain = kPosCap - 128 * kBigWin;  // drain before a step could overflow
 static_assert(kPosDrain > 0, "the block tier's hit queue must hold one step of hits");
 #ifndef TCB_SBWORDS
@@ -667,7 +674,7 @@ __device__ __forceinline__ void stream_group(const Segs& segs, const int32_t* __
 //     when its chunk index passes that end.
 // ncu (cfg 3, profiles/r18_*): resolution + masks were 24 of the 49 warp
 // instructions per window, the probes themselves 20.
-template <int kKind, int kLw, int kCap, class Segs, int kW>
+template <int kKind, int kLw, int kCap, class Segs, int kW, bool kPipe = TCB_BIG_INC_PIPE>
 __device__ __forceinline__ void stream_group_inc(const Segs& segs, const int32_t* __restrict__ pool, const Table& t,
                                                  int g0, int g1, int lane, int& npos, uint32_t& cnt, int4* segtab) {
   const unsigned FULL = 0xffffffffu;
@@ -725,20 +732,20 @@ __device__ __forceinline__ void stream_group_inc(const Segs& segs, const int32_t
   };
   load(0);
   for (int base = 0; base < total; base += 32 * kW) {
-#if TCB_BIG_INC_PIPE
-    int4 cur[kW];
+    if (kPipe) {  // the next windows' loads are issued before the current ones are probed
+      int4 cur[kW];
 #pragma unroll
-    for (int k = 0; k < kW; ++k) cur[k] = v[k];
-    if (base + 32 * kW < total) load(base + 32 * kW);
+      for (int k = 0; k < kW; ++k) cur[k] = v[k];
+      if (base + 32 * kW < total) load(base + 32 * kW);
 #pragma unroll
-    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, cur[k], 0xFu, lane, npos, cnt);
-    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
-#else
+      for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, cur[k], 0xFu, lane, npos, cnt);
+      if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+    } else {
 #pragma unroll
-    for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], 0xFu, lane, npos, cnt);
-    if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
-    if (base + 32 * kW < total) load(base + 32 * kW);
-#endif
+      for (int k = 0; k < kW; ++k) probe4<kKind, kLw, kCap>(t, v[k], 0xFu, lane, npos, cnt);
+      if (kKind == kBuckets && npos > kPosDrain) drain(t, npos, lane, cnt);
+      if (base + 32 * kW < total) load(base + 32 * kW);
+    }
   }
 }
 
@@ -1446,7 +1453,10 @@ __global__ void __launch_bounds__(kBigThreads, TCB_BIG_MINB) k_engine_big(Engine
           // and the wait at the next block barrier is at most one claim long
           const int g = ra + kBigClaim * gi;
           if (g >= rb) break;
-          if (kPadded && staged_exact)
+          if (kPadded && kExactOnly)  // no hit queue to bound the step: more windows in flight, pipelined
+            stream_group_inc<kExact, kLwBig, 1, Segs, kBigWinExact, TCB_BIG_EXACT_PIPE>(
+                segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane, npos, acc.cnt, segtab);
+          else if (kPadded && staged_exact)
             stream_group_inc<kExact, kLwBig, 1, Segs, kBigWin>(segs, a.pool, t, g + so, min(g + kBigClaim, rb) + so, lane,
                                                             npos, acc.cnt, segtab);
           else if (kPadded && !kExactOnly)
