@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(224, 6) k_gather(const int4* __restrict__ pool
 }
 
 int main(int argc, char** argv) {
-  const double pool_mb[] = {212, 2048};
-  const int Ls[] = {1, 2, 4, 6, 8, 16, 32, 64};
+  const double pool_mb[] = {106, 212, 2048};
+  const int Ls[] = {1, 2, 3, 4, 6, 8, 16, 32, 64};
   unsigned long long* out;
   CK(cudaMalloc(&out, 8));
   char* flush;
