@@ -240,7 +240,10 @@ int tc_count_lowest(const int64_t* eff_indptr, const int32_t* eff_indices, int64
 int tc_engine_timing(int32_t enable, double* total_ms_host, long long* launches_host, double* tier_ms_host);
 
 /* Engine tier caps (testing / tuning): key 0 = small warp-tier table cap
- * (0..128, default 128), key 2 = mid warp-tier cap (0..512, default 512),
+ * (0..256, default 128; 129..256 force the tier's wide form -- 8 ids of the
+ * owner's list per lane -- which the plan otherwise picks itself when the
+ * owners with 128 < d^ <= 256 carry a third of the engine's cost),
+ * key 2 = mid warp-tier cap (0..512, default 512),
  * key 1 = block-tier staged-table cap (0..4096, default 4096; larger tables
  * use binary search in global memory); value -1 restores a cap's default.
  * key 3 = pairs per chunk of tc_normalize_host's copy pipeline (>= 1,

@@ -18,7 +18,10 @@
 //          and holds the owner's list in registers (4 ids per lane): the
 //          rare filter hits are verified with one shuffle + one ballot, no
 //          bucket table is built; three windows per step are loaded
-//          straight into registers;
+//          straight into registers.  Wide form (k_small<.., 8>: d <= 256,
+//          8 ids per lane, two filter bits per id): the plan cuts the tiers
+//          at 256 instead of 128 when the owners with 128 < d <= 256 carry a
+//          third of the engine's cost (dense graphs: cfg 5 50.6 -> 45.6 ms);
 //   mid    (d <= 512): 8 KB slices (32K-bit two-bit filter + 2^8 buckets),
 //          4 warps per block, windows software-pipelined in registers;
 //   block  (d  > 512): a 512-thread block stages up to 4096 ids (256K-bit
@@ -819,6 +822,7 @@ __global__ void k_owner_desc(const int32_t* __restrict__ own, const int64_t* __r
 }
 
 // Runtime tier caps (tc_set_tuning; tests lower them to force every tier).
+static constexpr int kWideCap = 2 * kTabCap;  // the small tier's wide form (8 ids per lane)
 static int g_warp_cap = kTabCap;
 static int g_mid_cap = kMidCap;
 static int g_big_cap = kBigCap;
@@ -1120,7 +1124,7 @@ __device__ __forceinline__ void small_window(const int4* __restrict__ pool4, con
 
 // Filter (kExactT false: two bits per id in one hashed word) or exact bitmap
 // (ids in [tlo, tlo + span)) test of the 4 ids of v; returns the hit mask.
-template <bool kExactT, bool kPadded>
+template <bool kExactT, bool kPadded, int kFb = kSmallFb>
 __device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm, int32_t tlo, uint32_t span, int4 v,
                                                 uint32_t vm) {
   const int32_t xs[4] = {v.x, v.y, v.z, v.w};
@@ -1134,7 +1138,7 @@ __device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm,
     } else {
       const uint32_t h = tab_hash((uint32_t)xs[k]);
       const uint32_t wd = bm[h >> (32 - kLwS)];
-      if (kSmallFb == 2)
+      if (kFb == 2)
         m |= __funnelshift_r(wd, wd, h - k) & __funnelshift_r(wd, wd, (h >> 5) - k) & (1u << k);
       else
         m |= __funnelshift_r(wd, wd, h - k) & (1u << k);
@@ -1146,8 +1150,10 @@ __device__ __forceinline__ uint32_t small_probe(const uint32_t* __restrict__ bm,
 // Exact membership of the filter hits: the owner's list is held in
 // registers (lane l has ids l, l + 32, l + 64, l + 96; -1 pads), so each hit
 // (lane, id) is one shuffle, four compares and one ballot for the whole
-// warp.  Returns the number of true hits (warp-uniform).
-__device__ __forceinline__ uint32_t small_verify(uint32_t m, int4 v, int4 t, int lane) {
+// warp.  Returns the number of true hits (warp-uniform).  kIds = 8 (the wide
+// form, d <= 256): lane l also holds ids l + 128 .. l + 224 in t2.
+template <int kIds>
+__device__ __forceinline__ uint32_t small_verify(uint32_t m, int4 v, int4 t, int4 t2, int lane) {
   const unsigned FULL = 0xffffffffu;
   uint32_t c = 0;
   unsigned any = __ballot_sync(FULL, m != 0);
@@ -1156,21 +1162,23 @@ __device__ __forceinline__ uint32_t small_verify(uint32_t m, int4 v, int4 t, int
     const int k = __ffs(m) - 1;
     int x = (k == 0) ? v.x : (k == 1) ? v.y : (k == 2) ? v.z : v.w;
     x = __shfl_sync(FULL, x, src);
-    c += __ballot_sync(FULL, (t.x == x) | (t.y == x) | (t.z == x) | (t.w == x)) != 0u;
+    bool eq = (t.x == x) | (t.y == x) | (t.z == x) | (t.w == x);
+    if (kIds == 8) eq |= (t2.x == x) | (t2.y == x) | (t2.z == x) | (t2.w == x);
+    c += __ballot_sync(FULL, eq) != 0u;
     if (lane == src) m &= m - 1u;
     any = __ballot_sync(FULL, m != 0);
   }
   return c;
 }
 
-template <bool kExactT, bool kPadded>
-__device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int4 v,
+template <bool kExactT, bool kPadded, int kIds>
+__device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int4 t2, int4 v,
                                            uint32_t vm, int lane, uint32_t& cnt) {
-  const uint32_t m = small_probe<kExactT, kPadded>(bm, tlo, span, v, vm);
+  const uint32_t m = small_probe<kExactT, kPadded, (kIds == 8 ? 2 : kSmallFb)>(bm, tlo, span, v, vm);
   if (kExactT) {
     cnt += __popc(m);
   } else {
-    const uint32_t c = small_verify(m, v, t, lane);
+    const uint32_t c = small_verify<kIds>(m, v, t, t2, lane);
     if (lane == 0) cnt += c;
   }
 }
@@ -1179,10 +1187,10 @@ __device__ __forceinline__ void small_step(const uint32_t* bm, int32_t tlo, uint
 // kPadded: a tail segment (index nseg, starting at chunk `total`) maps the
 // chunks past the group's end onto the pool's INT32_MAX head, so window
 // lanes need no bounds check.
-template <bool kExactT, bool kPadded, class Segs>
+template <bool kExactT, bool kPadded, int kIds, class Segs>
 __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __restrict__ pool,
-                                            const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int g0, int g1,
-                                            int lane, uint32_t& cnt, int2* segtab, uint32_t* sbits) {
+                                            const uint32_t* bm, int32_t tlo, uint32_t span, int4 t, int4 t2, int g0,
+                                            int g1, int lane, uint32_t& cnt, int2* segtab, uint32_t* sbits) {
   const unsigned FULL = 0xffffffffu;
   constexpr int kW = TCB_SMALL_W;
   int s = 0, e = 0;
@@ -1249,7 +1257,7 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
       small_window<kPadded>(pool4, segtab, sbits, fast, lane_seg, excl, total, lane, base + 32 * (kW + k), cbase,
                             nv[k], nvm[k]);
 #pragma unroll
-    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded, kIds>(bm, tlo, span, t, t2, v[k], vm[k], lane, cnt);
 #pragma unroll
     for (int k = 0; k < kW; ++k) {
       v[k] = nv[k];
@@ -1257,7 +1265,7 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
     }
 #else
 #pragma unroll
-    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded>(bm, tlo, span, t, v[k], vm[k], lane, cnt);
+    for (int k = 0; k < kW; ++k) small_step<kExactT, kPadded, kIds>(bm, tlo, span, t, t2, v[k], vm[k], lane, cnt);
     if (base + 32 * kW < total) {
 #pragma unroll
       for (int k = 0; k < kW; ++k)
@@ -1273,8 +1281,9 @@ __device__ __forceinline__ void small_group(const Segs& segs, const int32_t* __r
   }
 }
 
-template <class Segs, bool kPadded>
+template <class Segs, bool kPadded, int kIds = 4>
 __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a, Segs segs) {
+  constexpr int kFb = kIds == 8 ? 2 : kSmallFb;  // the wide form holds up to 256 ids: two filter bits per id
   __shared__ uint32_t filts[kWarps][1 << kLwS];
   __shared__ int2 segtabs[kWarps][33];
   __shared__ uint32_t sbitss[kWarps][kSmallSbW];
@@ -1303,7 +1312,7 @@ __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a
       r = rb;
       const OwnerRef ow = resolve_owner(a, x);
       const int so = (int)ow.seg_off;
-      const int d = ow.d;  // <= 128
+      const int d = ow.d;  // <= 32 kIds
       acc.to_bucket(a, ow.u, lane);
       const int32_t* gtab = a.tab_indices + ow.t0;
       int4 t = make_int4(-1, -1, -1, -1);
@@ -1311,36 +1320,43 @@ __global__ void __launch_bounds__(kThreads, TCB_SMALL_MINB) k_small(EngineArgs a
       if (d > 32) t.y = lane + 32 < d ? __ldg(&gtab[lane + 32]) : -1;
       if (d > 64) t.z = lane + 64 < d ? __ldg(&gtab[lane + 64]) : -1;
       if (d > 96) t.w = lane + 96 < d ? __ldg(&gtab[lane + 96]) : -1;
+      int4 t2 = make_int4(-1, -1, -1, -1);
+      if (kIds == 8 && d > 128) {
+        t2.x = lane + 128 < d ? __ldg(&gtab[lane + 128]) : -1;
+        if (d > 160) t2.y = lane + 160 < d ? __ldg(&gtab[lane + 160]) : -1;
+        if (d > 192) t2.z = lane + 192 < d ? __ldg(&gtab[lane + 192]) : -1;
+        if (d > 224) t2.w = lane + 224 < d ? __ldg(&gtab[lane + 224]) : -1;
+      }
       const int32_t tlo = ow.tlo;
       const uint32_t span = ow.span;
-      const int32_t tv[4] = {t.x, t.y, t.z, t.w};
+      const int32_t tv[8] = {t.x, t.y, t.z, t.w, t2.x, t2.y, t2.z, t2.w};
       if (span < (32u << kLwS)) {
         // narrow id span: exact direct-mapped bitmap over [tlo, tlo + span)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kIds; ++k)
           if (tv[k] >= 0) {
             const uint32_t off = (uint32_t)(tv[k] - tlo);
             atomicOr(&bm[off >> 5], 1u << (off & 31));
           }
         __syncwarp();
         for (int g = ra; g < rb; g += 32)
-          small_group<true, kPadded>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt,
-                                     segtab, sbits);
+          small_group<true, kPadded, kIds>(segs, a.pool, bm, tlo, span, t, t2, g + so, min(g + 32, rb) + so, lane,
+                                           acc.cnt, segtab, sbits);
         __syncwarp();
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kIds; ++k)
           if (tv[k] >= 0) bm[(uint32_t)(tv[k] - tlo) >> 5] = 0;
       } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (tv[k] >= 0) filt_insert<kLwS, kSmallFb>(bm, tv[k]);
+        for (int k = 0; k < kIds; ++k)
+          if (tv[k] >= 0) filt_insert<kLwS, kFb>(bm, tv[k]);
         __syncwarp();
         for (int g = ra; g < rb; g += 32)
-          small_group<false, kPadded>(segs, a.pool, bm, tlo, span, t, g + so, min(g + 32, rb) + so, lane, acc.cnt,
-                                      segtab, sbits);
+          small_group<false, kPadded, kIds>(segs, a.pool, bm, tlo, span, t, t2, g + so, min(g + 32, rb) + so, lane,
+                                            acc.cnt, segtab, sbits);
         __syncwarp();
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kIds; ++k)
           if (tv[k] >= 0) filt_clear<kLwS>(bm, tv[k]);
       }
       __syncwarp();
@@ -1733,7 +1749,9 @@ __global__ void k_plan_seg(const int64_t* __restrict__ sp, int64_t nseg, const i
 __global__ void k_tier_flags(const int64_t* __restrict__ cp, int64_t x0, int64_t x1,
                              const int32_t* __restrict__ owner_map, const int64_t* __restrict__ tab_indptr,
                              int c0, int c1, int32_t* f0, int32_t* f1, int32_t* f2, unsigned long long* sizes) {
-  unsigned long long c[3] = {0, 0, 0};
+  // sizes[0..2]: owners per tier; sizes[3]: engine cost of the owners with c0 < d <= 2 c0 (the candidates of
+  // the small tier's wide form), sizes[4]: cost of all owners
+  unsigned long long c[5] = {0, 0, 0, 0, 0};
   GRID_STRIDE(i, x1 - x0 + 1) {
     int64_t x = x0 + i;
     int t = -1;
@@ -1741,13 +1759,16 @@ __global__ void k_tier_flags(const int64_t* __restrict__ cp, int64_t x0, int64_t
       int64_t u = owner_map ? (int64_t)owner_map[x] : x;
       int64_t d = tab_indptr[u + 1] - tab_indptr[u];
       t = (d <= c0) ? 0 : (d <= c1 ? 1 : 2);
+      const unsigned long long w = (unsigned long long)(cp[x + 1] - cp[x]);
+      c[4] += w;
+      if (d > c0 && d <= 2 * (int64_t)c0) c[3] += w;
     }
     f0[i] = t == 0;
     f1[i] = t == 1;
     f2[i] = t == 2;
     if (t >= 0) ++c[t];
   }
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 5; ++k) {
     unsigned long long v = c[k];
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sizes[k], v);
@@ -1821,6 +1842,7 @@ __global__ void k_max_span(const int4* __restrict__ desc_a, int64_t cnt, unsigne
 // run).  Built by prepare_engine, consumed by launch_engine.
 struct EngineLaunch {
   bool big_exact = false;  // every block-tier owner has an exact bitmap: launch the exact-only kernel
+  bool small_wide = false;  // the small tier takes d <= 256 (8 ids per lane, two filter bits)
   unsigned long long hsz[3] = {0, 0, 0};
   EngineArgs args[3];
   int* queue[3] = {nullptr, nullptr, nullptr};
@@ -1833,17 +1855,33 @@ EngineLaunch prepare_engine(Alloc& al, Scratch& tmp_sc, const int64_t* cp, const
                             const int32_t* owner_map = nullptr, int mode = 0, int parts = 1, int padded = 0) {
   const TierShape& ts = tier_shape();
   const int64_t nx = x1 - x0;
-  const int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
+  int c0 = g_warp_cap, c1 = std::max(g_mid_cap, g_warp_cap);
   const int grid = grid_for(nx + 1, 256, sm_count() * 16);
   EngineLaunch L;
+  L.small_wide = c0 > kTabCap;  // forced by tc_set_tuning(0, 129..256)
   int32_t* flag[3];
   for (int k = 0; k < 3; ++k) flag[k] = tmp_sc.alloc<int32_t>(nx + 1);
-  auto* sizes = tmp_sc.alloc<unsigned long long>(3);
-  TC_CUDA(cudaMemsetAsync(sizes, 0, 3 * sizeof(unsigned long long), s));
+  auto* sizes = tmp_sc.alloc<unsigned long long>(5);
+  unsigned long long hs[5] = {0, 0, 0, 0, 0};
+  TC_CUDA(cudaMemsetAsync(sizes, 0, 5 * sizeof(unsigned long long), s));
   k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2], sizes);
   check_launch();
-  TC_CUDA(cudaMemcpyAsync(L.hsz, sizes, sizeof(L.hsz), cudaMemcpyDeviceToHost, s));
+  TC_CUDA(cudaMemcpyAsync(hs, sizes, sizeof(hs), cudaMemcpyDeviceToHost, s));
   sync_stream(s);  // empty tiers are skipped entirely
+  if (TCB_SMALL_V20 && c0 == kTabCap && c1 >= kWideCap && 3 * hs[3] >= hs[4] && hs[3] > 0) {
+    // Dense graphs: when the owners with 128 < d <= 256 carry a third or more of the engine's cost, they run
+    // faster in the small tier's wide form than in the mid tier (cfg 5: 51.0 -> 47.5 ms; below that share the
+    // wide form's two-bit filter and longer verification cost the d <= 128 owners more than the move gains:
+    // cfg 3 14.1 -> 14.6 ms, cfg 2 1.60 -> 1.77 ms), so the tiers are cut again at 256.
+    c0 = kWideCap;
+    L.small_wide = true;
+    TC_CUDA(cudaMemsetAsync(sizes, 0, 5 * sizeof(unsigned long long), s));
+    k_tier_flags<<<grid, 256, 0, s>>>(cp, x0, x1, owner_map, tab_indptr, c0, c1, flag[0], flag[1], flag[2], sizes);
+    check_launch();
+    TC_CUDA(cudaMemcpyAsync(hs, sizes, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    sync_stream(s);
+  }
+  for (int k = 0; k < 3; ++k) L.hsz[k] = hs[k];
   size_t tmp = 0, tmp2 = 0;
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag[0], flag[0], nx + 1, s));
   TC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, (int64_t*)nullptr, (int64_t*)nullptr, nx + 1, s));
@@ -1927,8 +1965,14 @@ template <class Segs>
 static void launch_tier(EngineLaunch& L, int k, Segs segs, cudaStream_t s, const TierShape& ts) {
   if (k == 0) {
 #if TCB_SMALL_V20
-    if (L.args[0].padded) k_small<Segs, true><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
-    else k_small<Segs, false><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    if (L.small_wide) {
+      if (L.args[0].padded) k_small<Segs, true, 8><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+      else k_small<Segs, false, 8><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    } else if (L.args[0].padded) {
+      k_small<Segs, true><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    } else {
+      k_small<Segs, false><<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
+    }
 #else
     K_SMALL(Segs)<<<ts.blocks[0], kThreads, 0, s>>>(L.args[0], segs);
 #endif
@@ -2347,7 +2391,8 @@ int tc_set_tuning(int32_t key, int64_t value) {
     // value -1 restores a cap's default
     if (key == 0) {
       if (value == -1) value = tcb::kTabCap;
-      TC_REQUIRE(value >= 0 && value <= tcb::kTabCap, TC_EINVAL, "warp cap out of range");
+      // 129..256 force the small tier's wide form (8 ids per lane)
+      TC_REQUIRE(value >= 0 && value <= tcb::kWideCap, TC_EINVAL, "warp cap out of range");
       tcb::g_warp_cap = (int)value;
     } else if (key == 2) {
       if (value == -1) value = tcb::kMidCap;

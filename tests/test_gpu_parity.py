@@ -344,6 +344,51 @@ def test_engine_tiers_forced(caps):
         L.tc_set_tuning(1, -1)
 
 
+def _dense_er(n, p, seed):
+    rng = np.random.default_rng(seed)
+    iu = np.triu_indices(n, 1)
+    keep = rng.random(iu[0].shape[0]) < p
+    return np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.int64)
+
+
+@pytest.mark.parametrize("forced", [False, True])
+def test_small_tier_wide_form(forced):
+    """The small tier's wide form (owners with d^ <= 256: 8 ids of the list
+    per lane, two filter bits): picked by the plan itself on a dense graph
+    whose 128 < d^ <= 256 owners carry a third of the cost, and forced
+    through tc_set_tuning(0, 256) on the fixtures; totals, lowest-vertex
+    totals (non-padded segments) and surrogate partials against the oracle."""
+    from paper_1406_5687_b200 import _lib
+    L = _lib.lib()
+    raw = _dense_er(1400, 0.3, 21)
+    og = O.build_graph(*O.normalize(raw))
+    dd = og.eff_deg
+    assert int(((dd > 128) & (dd <= 256)).sum()) > 300 and int(dd.max()) > 256
+    T = O.count_triangles(og)
+    partials, _ = O.surrogate(og, O.balanced_bounds(O.node_costs(og, "predsum"), 0, og.n, 4))
+    try:
+        if forced:
+            _lib.check(L.tc_set_tuning(0, 256))
+        g = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(raw)))
+        assert tcb.count_triangles_seq(g) == T
+        assert int(count_lowest(g).item()) == T
+        total, rr = tcb.count_space_surrogate(g, 4)
+        assert total == T and [m.triangles for m in rr.metrics] == partials.tolist()
+        for parts in (2, 3):
+            assert sum(int(count_middle_part(g, q, parts).item()) for q in range(parts)) == T
+        if forced:
+            for name in ["pa_2000_10_3", "rmat_s10", "er_150_0.5_5", "gnm_2000_16000"]:
+                _, gs = graph_of(name)
+                Ts = int(SMALL[name]["T"][0])
+                assert tcb.count_triangles_seq(gs) == Ts, name
+                assert int(count_lowest(gs).item()) == Ts, name
+            _lib.check(L.tc_set_tuning(0, 200))  # a cap inside the wide range
+            g2 = tcb.build_graph(tcb.normalize(tcb.RawGraph.from_pairs(raw)))
+            assert tcb.count_triangles_seq(g2) == T
+    finally:
+        L.tc_set_tuning(0, -1)
+
+
 @pytest.mark.parametrize("name", SMALL_NAMES)
 def test_merge_path_engine(name):
     """The north star's literal formulation (warp per oriented edge, merge-path
