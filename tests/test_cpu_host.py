@@ -84,3 +84,21 @@ def test_no_cpu_fallback():
     raw = tcb.RawGraph.from_pairs([(0, 1), (1, 2), (0, 2)])
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         tcb.normalize(raw)
+
+
+def test_tuning_ranges():
+    """tc_set_tuning validates its caps on the host (no GPU work): the small
+    warp-tier cap accepts 0..256 (129..256 force the tier's wide form) and
+    rejects anything beyond; -1 restores the default."""
+    from paper_1406_5687_b200 import _lib
+    L = _lib.lib()
+    try:
+        for ok in (0, 8, 128, 129, 256):
+            assert L.tc_set_tuning(0, ok) == 0, ok
+        for bad in (257, 4096, -2):
+            assert L.tc_set_tuning(0, bad) != 0, bad
+        assert L.tc_set_tuning(2, 513) != 0 and L.tc_set_tuning(1, 4097) != 0
+        assert L.tc_set_tuning(9, 1) != 0
+    finally:
+        for key in (0, 2, 1):
+            assert L.tc_set_tuning(key, -1) == 0
